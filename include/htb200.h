@@ -1,0 +1,170 @@
+/*
+ * htb200.h -- C-ABI of the B200-native halftoning hot path (arXiv 2304.12152).
+ *
+ * Drop-in boundary for the reference package `htlab` (pure Python/NumPy,
+ * /root/reference/pkg/src/htlab).  Every entry point names the reference
+ * interface it replaces (file:line, relative to that directory).  The Python
+ * host layer `paper_2304_12152_b200` binds these with ctypes and mirrors the
+ * reference's Python API on top.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types.  Pointers named *_dev
+ *     are CUDA device pointers; `stream` is a cudaStream_t (NULL = legacy
+ *     default stream).  All kernels are sm_100a.
+ *   - every function returns an int status: HT_OK (0) or one of HT_E_*;
+ *     ht_last_error() returns the message of the last failure on the calling
+ *     thread.  The host layer maps HT_E_INVALID -> ValueError,
+ *     HT_E_NONFINITE -> FloatingPointError (nn.py:147-148), others ->
+ *     RuntimeError.
+ *   - images are row-major float32 (B, H, W) planes; the library never frees
+ *     caller memory.
+ *   - parameters are one flat float64 buffer in PolicyNetwork.params() order
+ *     (nn.py:118-122): conv_in.w (C,2,3,3), conv_in.b (C), then per residual
+ *     block conv1.w (C,C,3,3), conv1.b, conv2.w, conv2.b, then conv_out.w
+ *     (1,C,3,3), conv_out.b (1).  Weights are OIHW, cross-correlation
+ *     convention (nn.py:46-60).
+ */
+#ifndef HTB200_H
+#define HTB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HT_OK 0
+#define HT_E_INVALID 1     /* bad shape / argument  -> ValueError          */
+#define HT_E_NONFINITE 2   /* non-finite logits     -> FloatingPointError  */
+#define HT_E_CUDA 3        /* CUDA runtime failure  -> RuntimeError        */
+#define HT_E_UNSUPPORTED 4 /* arch / config not supported                  */
+
+/* ---- library ---------------------------------------------------------- */
+const char *ht_last_error(void);
+int ht_version(void);
+/* 1 if `device` is an sm_100 part this library's cubins run on. */
+int ht_device_supported(int device, int *supported);
+
+/* ---- host RNG: bit-exact xoshiro256++ / splitmix64 / Box-Muller ---------
+ * Replaces imagecore.Rng (imagecore.py:35-120) and gaussian_noise_map
+ * (imagecore.py:155-159) for host-side input preparation.  state[4] is the
+ * xoshiro state (Rng.state_words()). */
+int ht_rng_seed(uint64_t seed, uint64_t state[4]);            /* Rng.__init__ imagecore.py:43-50 */
+int ht_rng_uniforms(uint64_t state[4], int64_t n, double *out); /* Rng.uniforms imagecore.py:70-86 */
+int ht_rng_gaussians(uint64_t state[4], int64_t n, double *out);/* Rng.gaussians imagecore.py:88-99 */
+int ht_rng_gaussians_f32(uint64_t state[4], int64_t n, float *out);
+
+/* ---- policy network parameters ----------------------------------------- */
+/* Number of float64 parameters of PolicyNetwork(channels, blocks, in_ch=2). */
+int ht_num_params(int channels, int blocks, int64_t *n);
+/* Bytes of the packed device weight image produced by ht_pack_params. */
+int ht_packed_bytes(int channels, int blocks, int64_t *bytes);
+/* Repack the flat float64 parameters (device) into the kernels' layouts:
+ * fp32 OIHW + transposed/flipped copies for the SIMT training kernels and
+ * the fp16 UMMA K-major tiles of the fused tensor-core forward.  Must be
+ * re-run whenever the parameters change (Adam step, checkpoint load). */
+int ht_pack_params(const double *params_dev, int channels, int blocks,
+                   void *packed_dev, void *stream);
+
+/* ---- K1: fused inference forward + sigmoid + threshold ------------------
+ * Replaces PolicyNetwork.forward (nn.py:138-150) + rl.infer_halftone's
+ * threshold `p >= 0.5` (rl.py:306-311; L=2 twin multitone.py:61-67).
+ * c_dev/z_dev hold rows [in_row0, in_row0+in_rows) of B images of full
+ * height H and width W (image stride in_rows*W).  Produces rows
+ * [out_row0, out_row0+out_rows) (must lie inside the input rows, with a
+ * 34-row receptive-field halo available unless at a true image edge).
+ * Outputs (each optional, NULL to skip), image stride out_rows*W:
+ *   p_dev   float32 probabilities
+ *   h_dev   uint8 halftone, 1 = white (p >= 0.5)
+ *   pbm_dev PBM P4 payload bytes: per row ceil(W/8) bytes, bit 1 = black,
+ *           MSB first (imagecore.save_pbm, imagecore.py:289-297)
+ * workspace: ht_halftone_workspace_bytes() bytes of device scratch.
+ * impl: 0 = fused tcgen05 tensor-core kernel (default), 1 = fp32 SIMT
+ * layer-by-layer kernels (reference-precision cross-check).            */
+int ht_halftone_workspace_bytes(int channels, int blocks, int B, int H, int W,
+                                int in_rows, int out_rows, int impl,
+                                int64_t *bytes);
+int ht_halftone(const void *packed_dev, int channels, int blocks,
+                const float *c_dev, const float *z_dev, int B, int H, int W,
+                int in_row0, int in_rows, int out_row0, int out_rows,
+                float *p_dev, uint8_t *h_dev, uint8_t *pbm_dev,
+                void *workspace_dev, int64_t workspace_bytes, int impl,
+                void *stream);
+/* Reads the non-finite-logit flag the last ht_halftone left in `workspace_dev`
+ * (synchronises `stream`); HT_E_NONFINITE if set (nn.py:147-148). */
+int ht_halftone_check(const void *workspace_dev, void *stream);
+/* Number of kernel launches the last ht_halftone on this thread issued. */
+int ht_last_launch_count(int *count);
+
+/* ---- K1' / K2: training forward (stores activations) and backward -------
+ * Replaces PolicyNetwork.forward/backward (nn.py:138-160) incl.
+ * ResidualBlock (nn.py:91-100) and Conv2d (nn.py:46-77), fp32 math.
+ * x_dev: (B, 2, H, W) float32.  act_dev: ht_train_act_bytes() bytes.
+ * p_dev: (B, H, W) float32 output.  Returns HT_E_NONFINITE on non-finite
+ * logits (nn.py:147-148). */
+int ht_train_act_bytes(int channels, int blocks, int B, int H, int W,
+                       int64_t *bytes);
+int ht_policy_forward_train(const void *packed_dev, int channels, int blocks,
+                            const float *x_dev, int B, int H, int W,
+                            void *act_dev, float *p_dev, void *stream);
+/* dp_dev (B,H,W) float32 = dL/dp injected at the sigmoid output.
+ * grad_dev: flat float64 gradient in params() order, ACCUMULATED (+=) like
+ * the reference's .grad (nn.py:66-73; caller zeroes, nn.py:134-136).
+ * dx_dev (B,2,H,W) float32 or NULL. */
+int ht_policy_backward(const void *packed_dev, int channels, int blocks,
+                       const float *x_dev, int B, int H, int W,
+                       const void *act_dev, const float *p_dev,
+                       const float *dp_dev, double *grad_dev, float *dx_dev,
+                       void *stream);
+
+/* ---- K3 + K4: sampled actions, reward maps, LE flip-reward signal -------
+ * Replaces rl._sample_two_point (rl.py:67-69, L=2), metrics.RewardContext
+ * (metrics.py:165-204, region="full"), metrics.delta_map +
+ * _delta_cssim_map (metrics.py:333-392) and rl.le_signal (rl.py:96-109).
+ * p, c: (B,H,W) float32, u (B,H,W) float64 uniforms; m_out (B,H,W) float32
+ * sampled actions (u < p); stencils up to 11x11 (hvs_size default 11);
+ * signal_out (B,H,W) float32 = le_signal * scale; reward_out (B) float64
+ * scalar R per image.  k_hvs / w_ssim: ksize x ksize / wsize x wsize
+ * float64 stencils (host constants, hvs.py:54-103).                     */
+int ht_reward_le(const float *p_dev, const double *u_dev, const float *c_dev,
+                 int B, int H, int W, const double *k_hvs_dev, int ksize,
+                 const double *w_ssim_dev, int wsize, double w_s, double c1,
+                 double c2, double gain, double scale, float *m_out_dev,
+                 float *signal_out_dev, double *reward_out_dev,
+                 void *workspace_dev, int64_t workspace_bytes, void *stream);
+int ht_reward_workspace_bytes(int B, int H, int W, int64_t *bytes);
+
+/* ---- K5 / K7: spectral ---------------------------------------------------
+ * anisotropy_loss / anisotropy_loss_backward (spectral.py:100-133) for B
+ * images: loss_out (B) float64, grad_out (B,H,W) float32 = dL/dx * scale.
+ * ring_dev (H*W) int32 dense ring index (-1 = DC), counts_dev (n_rings)
+ * int32 (spectral.py:39-55).  grad_out may be NULL.                      */
+int ht_spectral_workspace_bytes(int B, int H, int W, int n_rings,
+                                int64_t *bytes);
+int ht_anisotropy(const float *x_dev, int B, int H, int W,
+                  const int32_t *ring_dev, const int32_t *counts_dev,
+                  int n_rings, double scale, double *loss_out_dev,
+                  float *grad_out_dev, void *workspace_dev,
+                  int64_t workspace_bytes, void *stream);
+/* rapsd (spectral.py:74-88) of the periodogram (spectral.py:17-24) of B
+ * images: power_out / anis_out (B, n_rings) float64, dc_out (B).        */
+int ht_rapsd(const float *x_dev, int B, int H, int W,
+             const int32_t *ring_dev, const int32_t *counts_dev, int n_rings,
+             double *power_out_dev, double *anis_out_dev, double *dc_out_dev,
+             void *workspace_dev, int64_t workspace_bytes, void *stream);
+
+/* ---- K6: Adam (nn.py:163-186) on the flat float64 parameter vector ----- */
+int ht_adam_step(double *params_dev, const double *grad_dev, double *m_dev,
+                 double *v_dev, int64_t n, int t, double lr, double beta1,
+                 double beta2, double eps, void *stream);
+
+/* ---- small device reductions used by rl.train_step (rl.py:254-255) ----- */
+/* out[0] += sum |p - rint(p)| over n elements (bin_gap numerator). */
+int ht_bin_gap_sum(const float *p_dev, int64_t n, double *out_dev,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HTB200_H */

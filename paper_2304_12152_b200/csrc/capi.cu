@@ -1,0 +1,122 @@
+// C-ABI plumbing: error strings, launch counting, device check and the
+// bit-exact host RNG (imagecore.py:14-120) used for input preparation.
+#include <math.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace ht {
+
+static thread_local char g_err[1024] = "";
+static thread_local int g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+void count_launch(int n) { g_launches += n; }
+void reset_launches() { g_launches = 0; }
+
+// ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
+static inline uint64_t splitmix64(uint64_t &s) {
+  s += 0x9E3779B97F4A7C15ull;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+static inline uint64_t xoshiro_next(uint64_t *s) {
+  const uint64_t out = rotl(s[0] + s[3], 23) + s[0];
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl(s[3], 45);
+  return out;
+}
+static inline double to_unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+}  // namespace ht
+
+extern "C" {
+
+const char *ht_last_error(void) { return ht::g_err; }
+int ht_version(void) { return 100; }
+
+int ht_last_launch_count(int *count) {
+  if (count) *count = ht::g_launches;
+  return HT_OK;
+}
+
+int ht_device_supported(int device, int *supported) {
+  cudaDeviceProp prop;
+  HT_CUDA(cudaGetDeviceProperties(&prop, device));
+  *supported = (prop.major == 10 && prop.minor == 0) ? 1 : 0;
+  return HT_OK;
+}
+
+// Rng.__init__ (imagecore.py:43-50): four splitmix64 outputs.
+int ht_rng_seed(uint64_t seed, uint64_t state[4]) {
+  uint64_t s = seed;
+  for (int i = 0; i < 4; ++i) state[i] = ht::splitmix64(s);
+  return HT_OK;
+}
+
+// Rng.uniforms (imagecore.py:70-86): (x >> 11) * 2^-53, row-major.
+int ht_rng_uniforms(uint64_t state[4], int64_t n, double *out) {
+  if (n < 0) return ht::fail(HT_E_INVALID, "n must be non-negative");
+  for (int64_t i = 0; i < n; ++i) out[i] = ht::to_unit(ht::xoshiro_next(state));
+  return HT_OK;
+}
+
+}  // extern "C"
+
+// Rng.gaussians (imagecore.py:88-99): Box-Muller on consumed pairs
+// (u1 = 1 - u_even, u2 = u_odd), r cos / r sin interleaved; odd n burns
+// the last sine.
+template <typename T>
+static int gaussians_impl(uint64_t state[4], int64_t n, T *out) {
+  if (n < 0) return ht::fail(HT_E_INVALID, "n must be non-negative");
+  const double two_pi = 2.0 * M_PI;
+  for (int64_t i = 0; i < n; i += 2) {
+    const double u0 = ht::to_unit(ht::xoshiro_next(state));
+    const double u1 = ht::to_unit(ht::xoshiro_next(state));
+    const double r = sqrt(-2.0 * log(1.0 - u0));
+    const double th = two_pi * u1;
+    out[i] = (T)(r * cos(th));
+    if (i + 1 < n) out[i + 1] = (T)(r * sin(th));
+  }
+  return HT_OK;
+}
+
+extern "C" {
+int ht_rng_gaussians(uint64_t state[4], int64_t n, double *out) {
+  return gaussians_impl<double>(state, n, out);
+}
+int ht_rng_gaussians_f32(uint64_t state[4], int64_t n, float *out) {
+  return gaussians_impl<float>(state, n, out);
+}
+
+int ht_num_params(int channels, int blocks, int64_t *n) {
+  if (channels < 1 || blocks < 0)
+    return ht::fail(HT_E_INVALID, "channels must be positive and blocks non-negative");
+  *n = ht::NetGeom(channels, blocks).total;
+  return HT_OK;
+}
+
+}  // extern "C"

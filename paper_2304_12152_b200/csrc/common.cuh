@@ -1,0 +1,81 @@
+// Shared helpers for the htb200 CUDA library: status/error plumbing and the
+// parameter-vector geometry of PolicyNetwork (nn.py:106-122).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/htb200.h"
+
+namespace ht {
+
+// thread-local last error message (ht_last_error)
+void set_error(const char *fmt, ...);
+int fail(int code, const char *fmt, ...);
+
+#define HT_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return ::ht::fail(HT_E_CUDA, "%s failed: %s (%s:%d)", #call,           \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);         \
+  } while (0)
+
+#define HT_CHECK_LAUNCH()                                                    \
+  do {                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                     \
+    if (e_ != cudaSuccess)                                                   \
+      return ::ht::fail(HT_E_CUDA, "kernel launch failed: %s (%s:%d)",       \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);         \
+  } while (0)
+
+#define HT_REQUIRE(cond, ...)                                                \
+  do {                                                                       \
+    if (!(cond)) return ::ht::fail(HT_E_INVALID, __VA_ARGS__);               \
+  } while (0)
+
+// per-thread launch counter (ht_last_launch_count)
+void count_launch(int n = 1);
+void reset_launches();
+
+// Offsets of the parameter tensors in the flat params() vector
+// (nn.py:118-122): conv_in, then per block conv1 / conv2, then conv_out.
+struct NetGeom {
+  int C, NB;
+  int64_t in_w, in_b;           // conv_in weight (C,2,3,3), bias (C)
+  int64_t blk0;                 // start of block 0
+  int64_t blk_stride;           // 2*(C*C*9 + C)
+  int64_t out_w, out_b;         // conv_out weight (1,C,3,3), bias (1)
+  int64_t total;
+  __host__ __device__ NetGeom(int C_, int NB_) : C(C_), NB(NB_) {
+    in_w = 0;
+    in_b = (int64_t)C * 2 * 9;
+    blk0 = in_b + C;
+    blk_stride = 2 * ((int64_t)C * C * 9 + C);
+    out_w = blk0 + blk_stride * NB;
+    out_b = out_w + (int64_t)C * 9;
+    total = out_b + 1;
+  }
+  __host__ __device__ int64_t w1(int b) const { return blk0 + blk_stride * b; }
+  __host__ __device__ int64_t b1(int b) const { return w1(b) + (int64_t)C * C * 9; }
+  __host__ __device__ int64_t w2(int b) const { return b1(b) + C; }
+  __host__ __device__ int64_t b2(int b) const { return w2(b) + (int64_t)C * C * 9; }
+};
+
+// Packed device weight image (ht_pack_params).  All sections 256-B aligned.
+//   f32     : fp32 copy of the flat params (SIMT forward, OIHW)
+//   f32t    : per conv, transposed + spatially flipped fp32 weights
+//             wt[ci][co][a][b] = w[co][ci][2-a][2-b] (dgrad as a forward conv)
+//   tc      : fp16 UMMA operand tiles for the fused forward (fwd_tc.cu)
+//   tcb     : fp32 biases for the fused forward
+struct PackLayout {
+  int64_t f32_off, f32t_off, tc_off, tcb_off, total;
+};
+PackLayout pack_layout(int C, int NB);
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+}  // namespace ht

@@ -1,0 +1,422 @@
+// FP32 SIMT convolution kernels: the training forward (activations kept for
+// backward), the backward (dgrad + wgrad), and the reference-precision
+// inference cross-check path (ht_halftone impl=1).
+//
+// Reference semantics: Conv2d.forward/backward (nn.py:46-77) -- 3x3
+// cross-correlation, stride 1, zero padding 1 applied to EVERY layer's input;
+// ResidualBlock (nn.py:91-100); PolicyNetwork (nn.py:138-160).  Tensors are
+// NCHW float32; gradients accumulate into a flat float64 vector in
+// params() order.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace ht {
+
+// ---------------------------------------------------------------------------
+// forward conv: out[b,co,y,x] = epi( bias[co] + sum_{ci,ky,kx}
+//                 x[b,ci,y+ky-1,x+kx-1] * w[co,ci,ky,kx] )
+// epi: mask-multiply (mask>0), residual add, relu -- in that order.  With
+// w = transposed+flipped weights and no bias this is the dgrad.
+constexpr int FT_X = 32, FT_Y = 8, F_CHUNK = 8;
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(128)
+conv3x3_fwd_kernel(const float *__restrict__ x, int H, int W,
+                   const float *__restrict__ w, const float *__restrict__ bias,
+                   const float *__restrict__ mask, const float *__restrict__ resid,
+                   float *__restrict__ out, int relu) {
+  constexpr int CC = CIN < F_CHUNK ? CIN : F_CHUNK;
+  constexpr int TXP = FT_X + 2, TYP = FT_Y + 2;
+  __shared__ float ws[CIN * 9 * COUT];       // [ci][ky][kx][co]
+  __shared__ float xs[CC][TYP][TXP + 1];
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * FT_X, y0 = blockIdx.y * FT_Y;
+  const int tid = threadIdx.x;
+  const int tx = (tid % 16) * 2, ty = tid / 16;  // 2 pixels per thread
+  for (int i = tid; i < CIN * 9 * COUT; i += 128) {
+    const int co = i % COUT, r = i / COUT;  // r = ci*9 + tap
+    ws[i] = w[(size_t)co * CIN * 9 + r];
+  }
+  float acc[2][COUT];
+#pragma unroll
+  for (int j = 0; j < COUT; ++j) acc[0][j] = acc[1][j] = 0.f;
+  const size_t plane = (size_t)H * W;
+  const float *xb = x + (size_t)b * CIN * plane;
+  for (int c0 = 0; c0 < CIN; c0 += CC) {
+    __syncthreads();
+    for (int i = tid; i < CC * TYP * TXP; i += 128) {
+      const int cc = i / (TYP * TXP), rem = i % (TYP * TXP);
+      const int yy = rem / TXP, xx = rem % TXP;
+      const int gy = y0 + yy - 1, gx = x0 + xx - 1;
+      float v = 0.f;
+      if (c0 + cc < CIN && gy >= 0 && gy < H && gx >= 0 && gx < W)
+        v = xb[(size_t)(c0 + cc) * plane + (size_t)gy * W + gx];
+      xs[cc][yy][xx] = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int cc = 0; cc < CC; ++cc) {
+      const int ci = c0 + cc;
+      if (ci >= CIN) break;
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        float xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[k] = xs[cc][ty + ky][tx + k];
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const float *wr = &ws[((ci * 3 + ky) * 3 + kx) * COUT];
+#pragma unroll
+          for (int co = 0; co < COUT; ++co) {
+            const float wv = wr[co];
+            acc[0][co] = fmaf(xv[kx], wv, acc[0][co]);
+            acc[1][co] = fmaf(xv[kx + 1], wv, acc[1][co]);
+          }
+        }
+      }
+    }
+  }
+  const int gy = y0 + ty;
+  if (gy >= H) return;
+  float *ob = out + (size_t)b * COUT * plane;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int gx = x0 + tx + k;
+    if (gx >= W) continue;
+    const size_t pix = (size_t)gy * W + gx;
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) {
+      float v = acc[k][co] + (bias ? bias[co] : 0.f);
+      const size_t idx = (size_t)b * COUT * plane + (size_t)co * plane + pix;
+      if (mask) v = mask[idx] > 0.f ? v : 0.f;
+      if (resid) v += resid[idx];
+      if (relu) v = fmaxf(v, 0.f);
+      ob[(size_t)co * plane + pix] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: dw[co,ci,ky,kx] += sum_{b,y,x} dout[b,co,y,x] * x[b,ci,y+ky-1,x+kx-1]
+//        db[co] += sum dout[b,co,:,:]     (nn.py:66-73)
+// One thread per (ci, tap); each CTA sweeps `tiles_per_cta` pixel tiles and
+// accumulates in fp32 registers, then atomically adds into the fp64 grads.
+constexpr int WT_X = 32, WT_Y = 8;
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(CIN * 9 < 64 ? 64 : CIN * 9)
+conv3x3_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dout,
+                     int B, int H, int W, int tiles_per_cta,
+                     double *__restrict__ dw, double *__restrict__ db) {
+  constexpr int NT = CIN * 9 < 64 ? 64 : CIN * 9;
+  constexpr int TXP = WT_X + 2, TYP = WT_Y + 2;
+  extern __shared__ float smem[];
+  float *xs = smem;                                  // [CIN][TYP][TXP]
+  float *ds = smem + CIN * TYP * TXP;                // [WT_Y*WT_X][COUT]
+  const int tid = threadIdx.x;
+  const bool active = tid < CIN * 9;
+  const int ci = tid / 9, tap = tid % 9, ky = tap / 3, kx = tap % 3;
+  float acc[COUT];
+  float bacc = 0.f;
+#pragma unroll
+  for (int j = 0; j < COUT; ++j) acc[j] = 0.f;
+  const int tx_n = (W + WT_X - 1) / WT_X, ty_n = (H + WT_Y - 1) / WT_Y;
+  const long total_tiles = (long)B * tx_n * ty_n;
+  const size_t plane = (size_t)H * W;
+  for (int it = 0; it < tiles_per_cta; ++it) {
+    const long t = (long)blockIdx.x * tiles_per_cta + it;
+    if (t >= total_tiles) break;
+    const int b = (int)(t / (tx_n * ty_n));
+    const int rem = (int)(t % (tx_n * ty_n));
+    const int y0 = (rem / tx_n) * WT_Y, x0 = (rem % tx_n) * WT_X;
+    __syncthreads();
+    for (int i = tid; i < CIN * TYP * TXP; i += NT) {
+      const int c = i / (TYP * TXP), r = i % (TYP * TXP);
+      const int yy = r / TXP, xx = r % TXP;
+      const int gy = y0 + yy - 1, gx = x0 + xx - 1;
+      float v = 0.f;
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W)
+        v = x[((size_t)b * CIN + c) * plane + (size_t)gy * W + gx];
+      xs[i] = v;
+    }
+    for (int i = tid; i < WT_Y * WT_X * COUT; i += NT) {
+      const int co = i % COUT, p = i / COUT;
+      const int gy = y0 + p / WT_X, gx = x0 + p % WT_X;
+      float v = 0.f;
+      if (gy < H && gx < W) v = dout[((size_t)b * COUT + co) * plane + (size_t)gy * W + gx];
+      ds[i] = v;
+    }
+    __syncthreads();
+    if (active) {
+      const float *xr = xs + ci * TYP * TXP + ky * TXP + kx;
+#pragma unroll 2
+      for (int p = 0; p < WT_Y * WT_X; ++p) {
+        const float xv = xr[(p / WT_X) * TXP + (p % WT_X)];
+        const float *dr = ds + p * COUT;
+#pragma unroll
+        for (int co = 0; co < COUT; ++co) acc[co] = fmaf(dr[co], xv, acc[co]);
+      }
+    }
+    if (tid < COUT) {
+      for (int p = 0; p < WT_Y * WT_X; ++p) bacc += ds[p * COUT + tid];
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int co = 0; co < COUT; ++co)
+      atomicAdd(&dw[((size_t)co * CIN + ci) * 9 + tap], (double)acc[co]);
+  }
+  if (tid < COUT) atomicAdd(&db[tid], (double)bacc);
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers
+__global__ void sigmoid_kernel(const float *__restrict__ logit, float *__restrict__ p,
+                               int64_t n, int *__restrict__ nonfinite) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float l = logit[i];
+  if (!isfinite(l)) atomicOr(nonfinite, 1);
+  p[i] = 1.f / (1.f + expf(-l));
+}
+
+// dlogits = dp * p * (1 - p)   (nn.py:156)
+__global__ void dlogit_kernel(const float *__restrict__ dp, const float *__restrict__ p,
+                              float *__restrict__ dl, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float q = p[i];
+  dl[i] = dp[i] * q * (1.f - q);
+}
+
+// window logits (B, in_rows, W) -> outputs for rows [out_row0, +out_rows):
+// p (float), h (uint8, p >= 0.5 <=> logit >= 0, rl.py:311)
+__global__ void threshold_window_kernel(const float *__restrict__ logit, int B, int in_rows,
+                                        int W, int row_off, int out_rows,
+                                        float *__restrict__ p, uint8_t *__restrict__ h,
+                                        int *__restrict__ nonfinite) {
+  const int64_t n = (int64_t)B * out_rows * W;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = (int)(i / ((int64_t)out_rows * W));
+  const int64_t rem = i % ((int64_t)out_rows * W);
+  const int y = (int)(rem / W), xx = (int)(rem % W);
+  const float l = logit[((int64_t)b * in_rows + y + row_off) * W + xx];
+  if (!isfinite(l)) atomicOr(nonfinite, 1);
+  if (p) p[i] = 1.f / (1.f + expf(-l));
+  if (h) h[i] = l >= 0.f ? 1 : 0;
+}
+
+}  // namespace ht
+
+// ===========================================================================
+// host orchestration
+namespace ht {
+
+template <int CIN, int COUT>
+static int conv_fwd(const float *x, int B, int H, int W, const float *w, const float *bias,
+                    const float *mask, const float *resid, float *out, int relu,
+                    cudaStream_t st) {
+  dim3 grid((W + FT_X - 1) / FT_X, (H + FT_Y - 1) / FT_Y, B);
+  conv3x3_fwd_kernel<CIN, COUT><<<grid, 128, 0, st>>>(x, H, W, w, bias, mask, resid, out, relu);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+template <int CIN, int COUT>
+static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, double *dw,
+                      double *db, cudaStream_t st) {
+  constexpr int NT = CIN * 9 < 64 ? 64 : CIN * 9;
+  const size_t smem = sizeof(float) * ((size_t)CIN * (WT_Y + 2) * (WT_X + 2) + WT_Y * WT_X * COUT);
+  static bool attr_set = false;
+  if (!attr_set) {
+    HT_CUDA(cudaFuncSetAttribute(conv3x3_wgrad_kernel<CIN, COUT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const long tiles = (long)B * ((W + WT_X - 1) / WT_X) * ((H + WT_Y - 1) / WT_Y);
+  const int per = tiles > 148 * 8 ? (int)((tiles + 148 * 8 - 1) / (148 * 8)) : 1;
+  const int grid = (int)((tiles + per - 1) / per);
+  conv3x3_wgrad_kernel<CIN, COUT><<<grid, NT, smem, st>>>(x, dout, B, H, W, per, dw, db);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+// Generic-C dispatch.  The fused tensor-core kernel is specialised for the
+// paper architecture (C=32, PRESET_PAPER nn.py:24); the SIMT path also
+// serves the mini preset (C=8, nn.py:25) used by the reference's tests.
+#define HT_DISPATCH_C(C, ...)                                                \
+  switch (C) {                                                               \
+    case 32: { constexpr int CC = 32; __VA_ARGS__; break; }                  \
+    case 8:  { constexpr int CC = 8;  __VA_ARGS__; break; }                  \
+    case 16: { constexpr int CC = 16; __VA_ARGS__; break; }                  \
+    case 4:  { constexpr int CC = 4;  __VA_ARGS__; break; }                  \
+    default: return ::ht::fail(HT_E_UNSUPPORTED, "channels=%d not compiled (supported: 4, 8, 16, 32)", C); \
+  }
+
+struct PackPtrs {
+  const float *f32, *f32t;
+};
+static PackPtrs pack_ptrs(const void *packed, int C, int NB) {
+  PackLayout L = pack_layout(C, NB);
+  const char *base = (const char *)packed;
+  return {(const float *)(base + L.f32_off), (const float *)(base + L.f32t_off)};
+}
+
+// Forward over (B, 2, H, W).  keep != nullptr: training mode, activations
+// stored as y[0..NB] and r[0..NB-1] (each B*C*H*W); else ping-pong scratch.
+static int simt_forward(const void *packed, int C, int NB, const float *x, int B, int H,
+                        int W, float *scratch, bool keep, float *logits, cudaStream_t st) {
+  NetGeom g(C, NB);
+  PackPtrs P = pack_ptrs(packed, C, NB);
+  const size_t act = (size_t)B * C * H * W;
+  auto ybuf = [&](int k) { return keep ? scratch + act * k : scratch + act * (k & 1); };
+  auto rbuf = [&](int k) { return keep ? scratch + act * (NB + 1 + k) : scratch + act * 2; };
+  int rc;
+  HT_DISPATCH_C(C, {
+    rc = conv_fwd<2, CC>(x, B, H, W, P.f32 + g.in_w, P.f32 + g.in_b, nullptr, nullptr,
+                         ybuf(0), 0, st);
+    if (rc) return rc;
+    for (int k = 0; k < NB; ++k) {
+      rc = conv_fwd<CC, CC>(ybuf(k), B, H, W, P.f32 + g.w1(k), P.f32 + g.b1(k), nullptr,
+                            nullptr, rbuf(k), 1, st);
+      if (rc) return rc;
+      rc = conv_fwd<CC, CC>(rbuf(k), B, H, W, P.f32 + g.w2(k), P.f32 + g.b2(k), nullptr,
+                            ybuf(k), ybuf(k + 1), 0, st);
+      if (rc) return rc;
+    }
+    rc = conv_fwd<CC, 1>(ybuf(NB), B, H, W, P.f32 + g.out_w, P.f32 + g.out_b, nullptr,
+                         nullptr, logits, 0, st);
+    if (rc) return rc;
+  });
+  return HT_OK;
+}
+
+int simt_halftone(const void *packed, int C, int NB, const float *c, const float *z, int B,
+                  int H, int W, int in_row0, int in_rows, int out_row0, int out_rows,
+                  float *p, uint8_t *h, void *ws, int64_t ws_bytes, int *nonfinite_dev,
+                  cudaStream_t st) {
+  const size_t plane = (size_t)in_rows * W;
+  const size_t act = (size_t)B * C * plane;
+  const int64_t need = (int64_t)sizeof(float) * (3 * act + (size_t)B * 2 * plane + (size_t)B * plane);
+  HT_REQUIRE(ws_bytes >= need, "workspace too small: %lld < %lld", (long long)ws_bytes,
+             (long long)need);
+  float *scratch = (float *)ws;
+  float *xin = scratch + 3 * act;
+  float *logits = xin + (size_t)B * 2 * plane;
+  // interleave (c, z) -> (B, 2, in_rows, W)
+  for (int b = 0; b < B; ++b) {
+    HT_CUDA(cudaMemcpyAsync(xin + (size_t)b * 2 * plane, c + (size_t)b * plane,
+                            plane * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    HT_CUDA(cudaMemcpyAsync(xin + (size_t)b * 2 * plane + plane, z + (size_t)b * plane,
+                            plane * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  int rc = simt_forward(packed, C, NB, xin, B, in_rows, W, scratch, false, logits, st);
+  if (rc) return rc;
+  const int64_t n = (int64_t)B * out_rows * W;
+  threshold_window_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      logits, B, in_rows, W, out_row0 - in_row0, out_rows, p, h, nonfinite_dev);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+int64_t simt_halftone_ws(int C, int B, int W, int in_rows) {
+  const size_t plane = (size_t)in_rows * W;
+  return (int64_t)sizeof(float) * (3 * (size_t)B * C * plane + (size_t)B * 3 * plane);
+}
+
+}  // namespace ht
+
+// ===========================================================================
+extern "C" {
+
+int ht_train_act_bytes(int channels, int blocks, int B, int H, int W, int64_t *bytes) {
+  const size_t act = (size_t)B * channels * H * W;
+  // y[0..NB], r[0..NB-1], logits, 3 backward temporaries
+  *bytes = (int64_t)sizeof(float) * ((2 * (size_t)blocks + 1) * act + (size_t)B * H * W + 3 * act);
+  return HT_OK;
+}
+
+int ht_policy_forward_train(const void *packed, int C, int NB, const float *x, int B, int H,
+                            int W, void *act, float *p, void *stream) {
+  HT_REQUIRE(B > 0 && H > 0 && W > 0, "input must be non-empty (B=%d H=%d W=%d)", B, H, W);
+  ht::reset_launches();
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t a = (size_t)B * C * H * W;
+  float *scratch = (float *)act;
+  float *logits = scratch + (2 * (size_t)NB + 1) * a;
+  int rc = ht::simt_forward(packed, C, NB, x, B, H, W, scratch, true, logits, st);
+  if (rc) return rc;
+  // sigmoid + finite check (nn.py:147-149)
+  int *d_flag;
+  HT_CUDA(cudaMallocAsync(&d_flag, sizeof(int), st));
+  HT_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  const int64_t n = (int64_t)B * H * W;
+  ht::sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(logits, p, n, d_flag);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
+  int hflag = 0;
+  HT_CUDA(cudaMemcpyAsync(&hflag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HT_CUDA(cudaFreeAsync(d_flag, st));
+  HT_CUDA(cudaStreamSynchronize(st));
+  if (hflag) return ht::fail(HT_E_NONFINITE, "non-finite logits");
+  return HT_OK;
+}
+
+int ht_policy_backward(const void *packed, int C, int NB, const float *x, int B, int H, int W,
+                       const void *act, const float *p, const float *dp, double *grad,
+                       float *dx, void *stream) {
+  HT_REQUIRE(B > 0 && H > 0 && W > 0, "input must be non-empty");
+  ht::reset_launches();
+  cudaStream_t st = (cudaStream_t)stream;
+  ht::NetGeom g(C, NB);
+  ht::PackPtrs P = ht::pack_ptrs(packed, C, NB);
+  const size_t a = (size_t)B * C * H * W;
+  const float *scratch = (const float *)act;
+  auto y = [&](int k) { return scratch + a * k; };
+  auto r = [&](int k) { return scratch + a * (NB + 1 + k); };
+  float *tmp = (float *)(scratch + (2 * (size_t)NB + 1) * a + (size_t)B * H * W);
+  float *dy = tmp, *dt = tmp + a, *dy2 = tmp + 2 * a;
+  // dlogits into dt's first plane-set (B*H*W floats)
+  float *dl = dt;
+  const int64_t n = (int64_t)B * H * W;
+  ht::dlogit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dp, p, dl, n);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
+  // transposed weights: f32t mirrors the f32 layout (same offsets)
+  int rc;
+  HT_DISPATCH_C(C, {
+    rc = ht::conv_wgrad<CC, 1>(y(NB), dl, B, H, W, grad + g.out_w, grad + g.out_b, st);
+    if (rc) return rc;
+    rc = ht::conv_fwd<1, CC>(dl, B, H, W, P.f32t + g.out_w, nullptr, nullptr, nullptr, dy, 0,
+                             st);
+    if (rc) return rc;
+    for (int k = NB - 1; k >= 0; --k) {
+      rc = ht::conv_wgrad<CC, CC>(r(k), dy, B, H, W, grad + g.w2(k), grad + g.b2(k), st);
+      if (rc) return rc;
+      rc = ht::conv_fwd<CC, CC>(dy, B, H, W, P.f32t + g.w2(k), nullptr, r(k), nullptr, dt, 0,
+                                st);
+      if (rc) return rc;
+      rc = ht::conv_wgrad<CC, CC>(y(k), dt, B, H, W, grad + g.w1(k), grad + g.b1(k), st);
+      if (rc) return rc;
+      rc = ht::conv_fwd<CC, CC>(dt, B, H, W, P.f32t + g.w1(k), nullptr, nullptr, dy, dy2, 0,
+                                st);
+      if (rc) return rc;
+      float *t = dy; dy = dy2; dy2 = t;
+    }
+    rc = ht::conv_wgrad<2, CC>(x, dy, B, H, W, grad + g.in_w, grad + g.in_b, st);
+    if (rc) return rc;
+    if (dx) {
+      rc = ht::conv_fwd<CC, 2>(dy, B, H, W, P.f32t + g.in_w, nullptr, nullptr, nullptr, dx, 0,
+                               st);
+      if (rc) return rc;
+    }
+  });
+  return HT_OK;
+}
+
+}  // extern "C"

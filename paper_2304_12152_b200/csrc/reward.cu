@@ -1,0 +1,256 @@
+// K3 + K4: action sampling, reward maps and the local-expectation (LE)
+// flip-reward signal, fp64 math (the training signal is ~1e-5 and must stay
+// within 1e-4 relative of the reference).
+//
+// Reference (region="full", binary policy L=2):
+//   sampling      m = (u < p)                          rl.py:67-69
+//   RewardContext f = conv(., k) (true convolution), window sums mu/E[..]
+//                 by correlation with the SSIM window w; sigma_c, SSIM,
+//                 CSSIM, reward map, scalar R         metrics.py:165-204, 95-107
+//   delta_map     dSSE = 2 d corr(e,k) + d^2 corr(1,k^2); dCS summed over the
+//                 window positions b covering a        metrics.py:333-392
+//   le_signal     signal = -sign * delta, sign = -1 where m = 1   rl.py:96-109
+// Since m is binary, E[h^2] = mu_h exactly (metrics.py:193 on a 0/1 map).
+#include "common.cuh"
+
+namespace ht {
+
+constexpr int RT = 16;            // output tile edge
+constexpr int RMAXK = 11;         // max stencil size supported (odd; the reference default is 11)
+constexpr int RH = RMAXK / 2;     // max halo
+
+__device__ __forceinline__ double ssim3(double mx, double my, double sxx, double syy, double sxy,
+                                        double c1, double c2) {
+  // metrics.py:95-107
+  const double vx = fmax(sxx - mx * mx, 0.0);
+  const double vy = fmax(syy - my * my, 0.0);
+  const double cov = sxy - mx * my;
+  const double sx = sqrt(vx), sy = sqrt(vy);
+  const double c3 = c2 / 2.0;
+  const double lum = (2.0 * mx * my + c1) / (mx * mx + my * my + c1);
+  const double con = (2.0 * sx * sy + c2) / (vx + vy + c2);
+  const double str = (cov + c3) / (sx * sy + c3);
+  return lum * con * str;
+}
+
+// Stage 1: per pixel maps.  Workspace layout per image (doubles, n = H*W):
+//   [0] e  [1] mu_h  [2] shc  [3] mu_c  [4] scc  [5] sigma_c  [6] ssim
+// plus per-image sums[2] = {sum e^2, sum cssim}.  Also writes m.
+__global__ void __launch_bounds__(256)
+reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
+                   const float *__restrict__ c, int H, int W, const double *__restrict__ k,
+                   int ks, const double *__restrict__ w, int wsz, double c1, double c2,
+                   double gain, double w_s, float *__restrict__ m_out, double *__restrict__ maps,
+                   double *__restrict__ sums) {
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
+  const int hk = ks / 2, hw = wsz / 2, hh = hk > hw ? hk : hw;
+  const int TP = RT + 2 * RH;
+  __shared__ double sm[RT + 2 * RH][RT + 2 * RH + 1];
+  __shared__ double sc[RT + 2 * RH][RT + 2 * RH + 1];
+  __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
+  __shared__ double red[2][8];
+  const size_t n = (size_t)H * W;
+  const float *pb = p + b * n;
+  const double *ub = u + b * n;
+  const float *cb = c + b * n;
+  for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
+  for (int i = threadIdx.x; i < wsz * wsz; i += 256) sw[i] = w[i];
+  for (int i = threadIdx.x; i < TP * TP; i += 256) {
+    const int yy = i / TP, xx = i % TP;
+    const int gy = y0 + yy - RH, gx = x0 + xx - RH;
+    double mv = 0.0, cv = 0.0;
+    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+      const size_t idx = (size_t)gy * W + gx;
+      mv = ub[idx] < (double)pb[idx] ? 1.0 : 0.0;
+      cv = (double)cb[idx];
+    }
+    sm[yy][xx] = mv;
+    sc[yy][xx] = cv;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
+  const int gy = y0 + ty, gx = x0 + tx;
+  double e2 = 0.0, cs = 0.0;
+  if (gy < H && gx < W) {
+    // f = conv(img, k): f[y,x] = sum_ij k[i,j] img[y-(i-hk), x-(j-hk)]
+    double fh = 0.0, fc = 0.0;
+    for (int i = 0; i < ks; ++i)
+      for (int j = 0; j < ks; ++j) {
+        const double kv = sk[i * ks + j];
+        const int yy = ty + RH - (i - hk), xx = tx + RH - (j - hk);
+        fh += kv * sm[yy][xx];
+        fc += kv * sc[yy][xx];
+      }
+    // window sums by correlation with w
+    double muh = 0.0, shc = 0.0, muc = 0.0, scc = 0.0;
+    for (int i = 0; i < wsz; ++i)
+      for (int j = 0; j < wsz; ++j) {
+        const double wv = sw[i * wsz + j];
+        const int yy = ty + RH + i - hw, xx = tx + RH + j - hw;
+        const double mv = sm[yy][xx], cv = sc[yy][xx];
+        muh += wv * mv;
+        shc += wv * (mv * cv);
+        muc += wv * cv;
+        scc += wv * (cv * cv);
+      }
+    const double sig = fmin(gain * sqrt(fmax(scc - muc * muc, 0.0)), 1.0);
+    const double s = ssim3(muh, muc, muh, scc, shc, c1, c2);
+    const double e = fh - fc;
+    const size_t idx = (size_t)gy * W + gx;
+    double *mb = maps + (size_t)b * 7 * n;
+    mb[0 * n + idx] = e;
+    mb[1 * n + idx] = muh;
+    mb[2 * n + idx] = shc;
+    mb[3 * n + idx] = muc;
+    mb[4 * n + idx] = scc;
+    mb[5 * n + idx] = sig;
+    mb[6 * n + idx] = s;
+    m_out[b * n + idx] = (float)sm[ty + RH][tx + RH];
+    e2 = e * e;
+    cs = sig * s + (1.0 - sig);
+  }
+  (void)hh;
+  for (int o = 16; o > 0; o >>= 1) {
+    e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    cs += __shfl_xor_sync(0xffffffffu, cs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = e2;
+    red[1][threadIdx.x >> 5] = cs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, bsum = 0.0;
+    for (int i = 0; i < 8; ++i) { a += red[0][i]; bsum += red[1][i]; }
+    atomicAdd(&sums[2 * b], a);
+    atomicAdd(&sums[2 * b + 1], bsum);
+  }
+}
+
+// Stage 2: delta for flipping every pixel, LE signal (scaled), per pixel a.
+__global__ void __launch_bounds__(256)
+reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ c, int H, int W,
+                 const double *__restrict__ k, int ks, const double *__restrict__ w, int wsz,
+                 double c1, double c2, double w_s, double scale, const double *__restrict__ maps,
+                 float *__restrict__ signal) {
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
+  const int hk = ks / 2, hw = wsz / 2;
+  constexpr int TP = RT + 2 * RH;
+  // b-side maps around the tile: e, mu_h, shc, mu_c, scc, sigma_c, ssim
+  __shared__ double sb[7][TP][TP];
+  __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
+  const size_t n = (size_t)H * W;
+  const double *mb = maps + (size_t)b * 7 * n;
+  for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
+  for (int i = threadIdx.x; i < wsz * wsz; i += 256) sw[i] = w[i];
+  for (int i = threadIdx.x; i < TP * TP; i += 256) {
+    const int yy = i / TP, xx = i % TP;
+    const int gy = y0 + yy - RH, gx = x0 + xx - RH;
+    const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+    const size_t idx = in ? (size_t)gy * W + gx : 0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) sb[q][yy][xx] = in ? mb[q * n + idx] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
+  const int gy = y0 + ty, gx = x0 + tx;
+  if (gy >= H || gx >= W) return;
+  const size_t ia = (size_t)gy * W + gx;
+  const double ma = (double)m_in[b * n + ia];
+  const double ca = (double)c[b * n + ia];
+  const double d = 1.0 - 2.0 * ma;  // other - h for a flip (+-1)
+  // dSSE = 2 d corr(e, k)[a] + d^2 sum_{y in image} k[y - a + hk]^2
+  double ce = 0.0, k2 = 0.0;
+  for (int i = 0; i < ks; ++i) {
+    const int yy = gy + i - hk;
+    if (yy < 0 || yy >= H) continue;
+    for (int j = 0; j < ks; ++j) {
+      const int xx = gx + j - hk;
+      if (xx < 0 || xx >= W) continue;
+      const double kv = sk[i * ks + j];
+      ce += kv * sb[0][ty + RH + i - hk][tx + RH + j - hk];
+      k2 += kv * kv;
+    }
+  }
+  const double dsse = 2.0 * d * ce + d * d * k2;
+  // dCS[a] = sum over window centres b = a - (dy,dx), in image, of
+  //          sigma_c[b] (SSIM_b(after) - SSIM_b(before)),  wd = w[hw+dy, hw+dx]
+  double dcs = 0.0;
+  if (w_s != 0.0) {
+    const double dh = 2.0 * ma * d + d * d;
+    for (int dy = -hw; dy <= hw; ++dy) {
+      const int by = gy - dy;
+      if (by < 0 || by >= H) continue;
+      for (int dx = -hw; dx <= hw; ++dx) {
+        const int bx = gx - dx;
+        if (bx < 0 || bx >= W) continue;
+        const double wd = sw[(hw + dy) * wsz + (hw + dx)];
+        const int sy = ty + RH - dy, sx = tx + RH - dx;
+        const double muh = sb[1][sy][sx], shc = sb[2][sy][sx], muc = sb[3][sy][sx];
+        const double scc = sb[4][sy][sx], sig = sb[5][sy][sx], s0 = sb[6][sy][sx];
+        const double s1 = ssim3(muh + wd * d, muc, muh + wd * dh, scc, shc + wd * d * ca, c1, c2);
+        dcs += sig * (s1 - s0);
+      }
+    }
+  }
+  const double delta = (-dsse + w_s * dcs) / (double)n;
+  // le_signal: -(sign * delta), sign = -1 where m == 1
+  const double sigv = ma == 1.0 ? delta : -delta;
+  signal[b * n + ia] = (float)(sigv * scale);
+}
+
+__global__ void reward_finalize_kernel(const double *__restrict__ sums, int B, double n,
+                                       double w_s, double *__restrict__ reward) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double mse = sums[2 * b] / n;
+  const double css = sums[2 * b + 1] / n;
+  reward[b] = -mse + w_s * css;
+}
+
+}  // namespace ht
+
+extern "C" {
+
+int ht_reward_workspace_bytes(int B, int H, int W, int64_t *bytes) {
+  *bytes = (int64_t)sizeof(double) * ((int64_t)B * 7 * H * W + 2 * (int64_t)B) + 256;
+  return HT_OK;
+}
+
+int ht_reward_le(const float *p, const double *u, const float *c, int B, int H, int W,
+                 const double *k, int ks, const double *w, int wsz, double w_s, double c1,
+                 double c2, double gain, double scale, float *m_out, float *signal_out,
+                 double *reward_out, void *ws, int64_t ws_bytes, void *stream) {
+  HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty batch");
+  HT_REQUIRE(ks % 2 == 1 && ks <= ht::RMAXK && wsz % 2 == 1 && wsz <= ht::RMAXK,
+             "stencils must be odd and at most %d wide", ht::RMAXK);
+  int64_t need = 0;
+  ht_reward_workspace_bytes(B, H, W, &need);
+  HT_REQUIRE(ws_bytes >= need, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  double *maps = (double *)ws;
+  double *sums = maps + (size_t)B * 7 * H * W;
+  HT_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 2 * B, st));
+  dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
+  ht::reward_maps_kernel<<<grid, 256, 0, st>>>(p, u, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s,
+                                               m_out, maps, sums);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
+  if (signal_out) {
+    ht::reward_le_kernel<<<grid, 256, 0, st>>>(m_out, c, H, W, k, ks, w, wsz, c1, c2, w_s, scale,
+                                                maps, signal_out);
+    ht::count_launch();
+    HT_CHECK_LAUNCH();
+  }
+  if (reward_out) {
+    ht::reward_finalize_kernel<<<(B + 127) / 128, 128, 0, st>>>(sums, B, (double)H * W, w_s,
+                                                                 reward_out);
+    ht::count_launch();
+    HT_CHECK_LAUNCH();
+  }
+  return HT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,332 @@
+"""Policy network, Adam and the cosine schedule -- htlab.nn drop-in (nn.py:28-199).
+
+The object model mirrors the reference: `PolicyNetwork(channels, blocks,
+in_channels)` with `.conv_in`, `.res[i].conv1/.conv2`, `.conv_out`, and
+`params()` returning `Parameter`s whose `.value` / `.grad` are float64 numpy
+arrays in the reference order (nn.py:118-122).  Those host arrays stay the
+API surface; the network keeps a device copy (flat float64 + the packed
+kernel layouts of ht_pack_params) that is re-synchronised whenever the host
+values change, and device-side updates (GPU Adam in rl.train_step) are
+written back to the host arrays.
+
+Compute:
+  forward / backward   fp32 SIMT CUDA kernels, activations kept on the
+                       device between the two calls (nn.py:138-160)
+  halftone_device      the fused tcgen05 kernel K1 (inference hot path)
+"""
+
+import math
+
+import numpy as np
+
+from . import _lib
+
+PRESET_PAPER = (32, 16)
+PRESET_MINI = (8, 2)
+
+
+class Parameter:
+    """nn.py:28-33."""
+    __slots__ = ("value", "grad")
+
+    def __init__(self, value):
+        self.value = np.asarray(value, dtype=np.float64)
+        self.grad = np.zeros_like(self.value)
+
+
+class Conv2d:
+    """Parameter container of a 3x3 / stride 1 / zero-pad 1 conv (nn.py:36-80)."""
+
+    def __init__(self, c_in, c_out):
+        self.c_in, self.c_out = c_in, c_out
+        self.weight = Parameter(np.zeros((c_out, c_in, 3, 3)))
+        self.bias = Parameter(np.zeros(c_out))
+
+    def params(self):
+        return [self.weight, self.bias]
+
+
+class ResidualBlock:
+    """x + conv2(relu(conv1(x))) (nn.py:83-103)."""
+
+    def __init__(self, channels):
+        self.conv1 = Conv2d(channels, channels)
+        self.conv2 = Conv2d(channels, channels)
+
+    def params(self):
+        return self.conv1.params() + self.conv2.params()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class PolicyNetwork:
+    """Input conv (2 -> C), B residual blocks, output conv (C -> 1), sigmoid."""
+
+    def __init__(self, channels=32, blocks=16, in_channels=2):
+        if in_channels != 2:
+            raise ValueError("the policy network takes (contone, noise): in_channels must be 2")
+        if channels < 1 or blocks < 0:
+            raise ValueError("channels must be positive and blocks non-negative")
+        self.channels, self.blocks, self.in_channels = channels, blocks, in_channels
+        self.conv_in = Conv2d(in_channels, channels)
+        self.res = [ResidualBlock(channels) for _ in range(blocks)]
+        self.conv_out = Conv2d(channels, 1)
+        self._params = self.params()
+        self._dev = None            # torch.device
+        self._flat = None           # float64 device params
+        self._packed = None         # uint8 device packed weights
+        self._uploaded = None       # host flat copy matching the device
+        self._cache = None          # training forward state (x, act, p, B, H, W)
+
+    # ------------------------------------------------------------------ host API
+    def params(self):
+        out = self.conv_in.params()
+        for blk in self.res:
+            out += blk.params()
+        return out + self.conv_out.params()
+
+    def num_params(self):
+        return sum(p.value.size for p in self._params)
+
+    def init_params(self, rng, std=0.01):
+        """nn.py:124-132: weights N(0, std^2) drawn in params() order, biases 0."""
+        for p in self._params:
+            if p.value.ndim > 1:
+                p.value[...] = rng.gaussians(p.value.size).reshape(p.value.shape) * std
+            else:
+                p.value[...] = 0.0
+            p.grad[...] = 0.0
+
+    def zero_grad(self):
+        for p in self._params:
+            p.grad[...] = 0.0
+
+    def flat_values(self):
+        return np.concatenate([p.value.ravel() for p in self._params])
+
+    def set_flat_values(self, flat):
+        at = 0
+        for p in self._params:
+            n = p.value.size
+            p.value[...] = np.asarray(flat[at:at + n]).reshape(p.value.shape)
+            at += n
+
+    # ------------------------------------------------------------------ device state
+    def to(self, device):
+        torch = _torch()
+        self._dev = torch.device(device)
+        self._flat = None
+        self._uploaded = None
+        return self
+
+    @property
+    def device(self):
+        if self._dev is None:
+            _lib.require_cuda()
+            torch = _torch()
+            self._dev = torch.device("cuda", torch.cuda.current_device())
+        return self._dev
+
+    def sync(self, force=False):
+        """Upload + repack if the host parameter values changed."""
+        torch = _torch()
+        flat = self.flat_values()
+        if (not force and self._flat is not None and self._uploaded is not None
+                and np.array_equal(flat, self._uploaded)):
+            return
+        dev = self.device
+        with torch.cuda.device(dev):
+            if self._flat is None:
+                self._flat = torch.empty(flat.size, dtype=torch.float64, device=dev)
+                nbytes = _lib.out_i64("ht_packed_bytes", self.channels, self.blocks)
+                self._packed = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self._flat.copy_(torch.from_numpy(flat))
+            self._repack()
+        self._uploaded = flat
+
+    def _repack(self):
+        _lib.call("ht_pack_params", _lib.ptr(self._flat), self.channels, self.blocks,
+                  _lib.ptr(self._packed), _lib.stream_ptr())
+
+    def device_flat(self):
+        self.sync()
+        return self._flat
+
+    def packed(self):
+        self.sync()
+        return self._packed
+
+    def pull_from_device(self):
+        """Device params (after a device-side update) -> host arrays."""
+        flat = self._flat.detach().cpu().numpy().copy()
+        self.set_flat_values(flat)
+        self._uploaded = flat
+        self._repack()
+
+    # ------------------------------------------------------------------ compute
+    def forward(self, x):
+        """nn.py:138-150: probabilities (B, 1, H, W) float64; keeps the
+        activations on the device for backward()."""
+        torch = _torch()
+        x = np.asarray(x, dtype=np.float64)
+        if x.ndim != 4:
+            raise ValueError("input must be (batch, channels, height, width)")
+        if x.shape[1] != self.in_channels:
+            raise ValueError(f"expected {self.in_channels} input channels, got {x.shape[1]}")
+        xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(self.device)
+        p = self.forward_device(xd)
+        return p.double().cpu().numpy()[:, None]
+
+    def forward_device(self, x):
+        """Training forward on a device tensor x (B, 2, H, W) float32 ->
+        p (B, H, W) float32 device tensor; activations cached."""
+        torch = _torch()
+        _lib.require_cuda()
+        self.sync()
+        if x.dim() != 4 or x.shape[1] != self.in_channels:
+            raise ValueError("input must be (batch, 2, height, width)")
+        B, _, H, W = x.shape
+        if B == 0 or H == 0 or W == 0:
+            raise ValueError("input must be non-empty")
+        x = x.contiguous().float()
+        nbytes = _lib.out_i64("ht_train_act_bytes", self.channels, self.blocks, B, H, W)
+        act = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+        p = torch.empty((B, H, W), dtype=torch.float32, device=x.device)
+        self._cache = None
+        _lib.call("ht_policy_forward_train", _lib.ptr(self._packed), self.channels, self.blocks,
+                  _lib.ptr(x), B, H, W, _lib.ptr(act), _lib.ptr(p), _lib.stream_ptr())
+        self._cache = (x, act, p, B, H, W)
+        return p
+
+    def backward(self, dp):
+        """nn.py:152-160: accumulate parameter grads into .grad, return dL/dx."""
+        torch = _torch()
+        if self._cache is None:
+            raise RuntimeError("backward() needs a preceding forward()")
+        x, act, p, B, H, W = self._cache
+        dp = np.asarray(dp, dtype=np.float64).reshape(B, H, W)
+        dpd = torch.from_numpy(np.ascontiguousarray(dp, dtype=np.float32)).to(x.device)
+        grad = torch.zeros(self.num_params(), dtype=torch.float64, device=x.device)
+        dx = torch.empty((B, 2, H, W), dtype=torch.float32, device=x.device)
+        self.backward_device(dpd, grad, dx)
+        g = grad.cpu().numpy()
+        at = 0
+        for prm in self._params:
+            n = prm.value.size
+            prm.grad += g[at:at + n].reshape(prm.value.shape)
+            at += n
+        return dx.double().cpu().numpy()
+
+    def backward_device(self, dp, grad, dx=None):
+        """Device backward: dp (B,H,W) fp32; grad (flat fp64) accumulated."""
+        if self._cache is None:
+            raise RuntimeError("backward() needs a preceding forward()")
+        x, act, p, B, H, W = self._cache
+        _lib.call("ht_policy_backward", _lib.ptr(self._packed), self.channels, self.blocks,
+                  _lib.ptr(x), B, H, W, _lib.ptr(act), _lib.ptr(p), _lib.ptr(dp.contiguous()),
+                  _lib.ptr(grad), _lib.ptr(dx), _lib.stream_ptr())
+
+    def halftone_device(self, c, z, p_out=None, h_out=None, pbm_out=None, impl=None,
+                        rows=None, workspace=None, check=False, stream=None):
+        """Fused inference forward + threshold (K1) on device tensors.
+
+        c, z: (B, in_rows, W) float32 contone / noise (rows [in_row0,
+        in_row0+in_rows) of images of height H: rows=(H, in_row0, out_row0,
+        out_rows), default the whole image).  Outputs (B, out_rows, W):
+        p_out float32, h_out uint8 (1 = white), pbm_out PBM P4 payload
+        (B, out_rows, ceil(W/8)).  impl 0 = tcgen05 fused kernel (default for
+        the paper architecture), 1 = fp32 SIMT cross-check path."""
+        torch = _torch()
+        self.sync()
+        if c.dim() == 2:
+            c, z = c[None], z[None]
+        B, in_rows, W = c.shape
+        if z.shape != c.shape:
+            raise ValueError("contone and noise shapes differ")
+        if rows is None:
+            rows = (in_rows, 0, 0, in_rows)
+        H, in_row0, out_row0, out_rows = rows
+        if impl is None:
+            impl = 0 if self.channels == 32 else 1
+        nbytes = _lib.out_i64("ht_halftone_workspace_bytes", self.channels, self.blocks, B, H, W,
+                              in_rows, out_rows, impl)
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = torch.empty(nbytes, dtype=torch.uint8, device=c.device)
+        sp = _lib.stream_ptr(stream)
+        _lib.call("ht_halftone", _lib.ptr(self._packed), self.channels, self.blocks,
+                  _lib.ptr(c.contiguous()), _lib.ptr(z.contiguous()), B, H, W, in_row0, in_rows,
+                  out_row0, out_rows, _lib.ptr(p_out), _lib.ptr(h_out), _lib.ptr(pbm_out),
+                  _lib.ptr(workspace), nbytes, impl, sp)
+        if check:
+            _lib.call("ht_halftone_check", _lib.ptr(workspace), sp)
+        return workspace
+
+
+class Adam:
+    """Bias-corrected Adam (nn.py:163-186), run on the device (K6)."""
+
+    def __init__(self, params, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.params = list(params)
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.t = 0
+        self.m = [np.zeros_like(p.value) for p in self.params]
+        self.v = [np.zeros_like(p.value) for p in self.params]
+        self._dm = self._dv = None
+
+    def _device_state(self, dev):
+        torch = _torch()
+        if self._dm is None:
+            self._dm = torch.from_numpy(np.concatenate([m.ravel() for m in self.m])).to(dev)
+            self._dv = torch.from_numpy(np.concatenate([v.ravel() for v in self.v])).to(dev)
+        return self._dm, self._dv
+
+    def step_device(self, flat, grad, lr):
+        """One Adam step on device tensors (flat params, flat grads, fp64)."""
+        m, v = self._device_state(flat.device)
+        self.t += 1
+        _lib.call("ht_adam_step", _lib.ptr(flat), _lib.ptr(grad), _lib.ptr(m), _lib.ptr(v),
+                  flat.numel(), self.t, float(lr), self.beta1, self.beta2, self.eps,
+                  _lib.stream_ptr())
+
+    def pull_state(self):
+        """Device moments -> the host lists (checkpointing / inspection)."""
+        if self._dm is None:
+            return
+        mh, vh = self._dm.cpu().numpy(), self._dv.cpu().numpy()
+        at = 0
+        for m, v in zip(self.m, self.v):
+            n = m.size
+            m[...] = mh[at:at + n].reshape(m.shape)
+            v[...] = vh[at:at + n].reshape(v.shape)
+            at += n
+
+    def step(self, lr):
+        """nn.py:175-186 on the parameters' host .value/.grad (uploads, runs
+        the device kernel, writes back)."""
+        torch = _torch()
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        flat = torch.from_numpy(np.concatenate([p.value.ravel() for p in self.params])).to(dev)
+        grad = torch.from_numpy(np.concatenate([p.grad.ravel() for p in self.params])).to(dev)
+        self.step_device(flat, grad, lr)
+        fh = flat.cpu().numpy()
+        at = 0
+        for p in self.params:
+            n = p.value.size
+            p.value[...] = fh[at:at + n].reshape(p.value.shape)
+            at += n
+        self.pull_state()
+
+
+def cosine_lr(t, total, lr_start=3e-4, lr_end=1e-5):
+    """nn.py:189-199."""
+    if total <= 0:
+        raise ValueError("total steps must be positive")
+    if t >= total:
+        return lr_end
+    if t < 0:
+        raise ValueError("step must be non-negative")
+    return float(lr_end + 0.5 * (lr_start - lr_end) * (1.0 + math.cos(math.pi * t / total)))

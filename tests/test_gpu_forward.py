@@ -1,0 +1,157 @@
+"""GPU parity of the inference hot path (K1) against the reference oracle.
+
+Tolerance (BASELINE.json north_star): probabilities within 1e-3 absolute of
+the reference; halftones bit-exact except where the reference probability
+lies within 1e-3 of the 0.5 threshold.  The fp32 SIMT path (impl=1) is held
+to 2e-5.  Tiling / batching / row-window sharding of the fused kernel must
+be BITWISE invariant (every pixel sees the same operation sequence).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+P_TOL = 1e-3       # north_star: probabilities within 1e-3 absolute
+BAND = 1e-3        # threshold exemption band
+
+
+def _net(std, ch=32, nb=16, seed=0):
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(ch, nb)
+    net.init_params(Rng(seed), std=std)
+    return net
+
+
+def _check(p, h, p_ref, tol):
+    p_ref = np.asarray(p_ref, np.float64)
+    err = np.abs(p - p_ref)
+    assert err.max() <= tol, f"max|dp| = {err.max():.3e}"
+    h_ref = (p_ref >= 0.5)
+    outside = np.abs(p_ref - 0.5) >= BAND
+    assert np.array_equal(h[outside].astype(bool), h_ref[outside])
+    return float(err.max()), float(1.0 - outside.mean())
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("std", [0.01, 0.05])
+def test_config1_256(impl, std):
+    from paper_2304_12152_b200 import rl
+    g = golden("forward.npz")
+    net = _net(std)
+    h, p = rl.halftone(net, g["cfg1_c"], g["cfg1_z"], impl=impl)
+    err, band = _check(p, h, g[f"cfg1_p_std{std}"], P_TOL if impl == 0 else 2e-5)
+    print(f"impl={impl} std={std}: max|dp|={err:.3e} band={band:.4f}")
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("shape", ["1x1", "3x5", "7x2", "37x131"])
+def test_ragged_shapes(impl, shape):
+    from paper_2304_12152_b200 import rl
+    g = golden("forward.npz")
+    net = _net(0.05)
+    h, p = rl.halftone(net, g[f"rag_{shape}_c"], g[f"rag_{shape}_z"], impl=impl)
+    _check(p, h, g[f"rag_{shape}_p"], P_TOL if impl == 0 else 2e-5)
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("std", [0.01, 0.05])
+def test_small_full_arch(impl, std):
+    from paper_2304_12152_b200 import rl
+    g = golden("forward.npz")
+    h, p = rl.halftone(_net(std), g["small_c"], g["small_z"], impl=impl)
+    _check(p, h, g[f"small_p_std{std}"], P_TOL if impl == 0 else 2e-5)
+
+
+def test_mini_arch_simt():
+    from paper_2304_12152_b200 import rl
+    g = golden("forward.npz")
+    h, p = rl.halftone(_net(0.05, 8, 2), g["small_c"], g["small_z"])  # C=8 -> SIMT
+    _check(p, h, g["small_p_mini"], 2e-5)
+
+
+def test_batch_equals_single_bitwise():
+    import torch
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05)
+    cs = synth.config_batch(3, 70, 90, seed=3, step_frac=0.34)
+    zs = np.stack([gaussian_noise_map_f32(Rng(10 + i), 90, 70) for i in range(3)])
+    hb, pb = rl.halftone(net, cs, zs)
+    for i in range(3):
+        hi, pi = rl.halftone(net, cs[i], zs[i])
+        assert np.array_equal(pi, pb[i]) and np.array_equal(hi, hb[i])
+
+
+def test_row_window_sharding_bitwise():
+    """Config-4 style row strips with the 34-row receptive-field halo."""
+    import torch
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05)
+    H, W = 200, 150
+    c = torch.from_numpy(synth.contone(H, W, seed=9)).cuda()
+    z = torch.from_numpy(gaussian_noise_map_f32(Rng(4), W, H)).cuda()
+    full = torch.empty((1, H, W), device="cuda")
+    net.halftone_device(c[None], z[None], p_out=full)
+    halo = 34
+    parts = []
+    for r0, r1 in ((0, 70), (70, 151), (151, 200)):
+        i0, i1 = max(0, r0 - halo), min(H, r1 + halo)
+        out = torch.empty((1, r1 - r0, W), device="cuda")
+        net.halftone_device(c[None, i0:i1].contiguous(), z[None, i0:i1].contiguous(), p_out=out,
+                            rows=(H, i0, r0, r1 - r0))
+        parts.append(out)
+    stitched = torch.cat(parts, dim=1)
+    assert torch.equal(stitched, full)
+
+
+def test_pbm_payload_matches_packbits():
+    import torch
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05)
+    H, W = 33, 77
+    c = torch.from_numpy(synth.contone(H, W, seed=2)).cuda()[None]
+    z = torch.from_numpy(gaussian_noise_map_f32(Rng(2), W, H)).cuda()[None]
+    h = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
+    pbm = torch.empty((1, H, (W + 7) // 8), dtype=torch.uint8, device="cuda")
+    net.halftone_device(c, z, h_out=h, pbm_out=pbm)
+    hh = h.cpu().numpy()[0]
+    want = np.packbits((1 - hh).astype(np.uint8), axis=1)     # imagecore.py:293-294
+    assert np.array_equal(pbm.cpu().numpy()[0], want)
+
+
+def test_nonfinite_logits_raise():
+    from paper_2304_12152_b200 import rl
+    net = _net(0.05)
+    net.conv_out.bias.value[0] = np.inf
+    with pytest.raises(FloatingPointError):
+        rl.halftone(net, np.full((8, 8), 0.5), np.zeros((8, 8)))
+
+
+def test_infer_halftone_uses_reference_noise_draws():
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    net = _net(0.05)
+    c = np.linspace(0, 1, 24 * 20).reshape(24, 20)
+    h, p = rl.infer_halftone(net, c, Rng(17))
+    params = O.init_params(O.Rng(0), 32, 16, 2, 0.05)
+    z = O.gaussian_noise_map(O.Rng(17), 20, 24)
+    _, p_ref = O.halftone(params, c.astype(np.float32), z.astype(np.float32))
+    _check(p, h, p_ref, P_TOL)
+
+
+def test_device_api_without_sync_reuses_packed_weights():
+    """Parameter edits on the host are picked up before the next forward."""
+    from paper_2304_12152_b200 import rl
+    net = _net(0.05)
+    c, z = np.full((16, 16), 0.3), np.zeros((16, 16))
+    _, p1 = rl.halftone(net, c, z)
+    net.conv_out.bias.value[0] += 1.0
+    _, p2 = rl.halftone(net, c, z)
+    assert np.all(p2 > p1)
