@@ -96,6 +96,12 @@ int ht_halftone(const void *packed_dev, int channels, int blocks,
 int ht_halftone_check(const void *workspace_dev, void *stream);
 /* Number of kernel launches the last ht_halftone on this thread issued. */
 int ht_last_launch_count(int *count);
+/* Measurement hooks (bench.py): when enabled, every fused-forward pass launch
+ * on this thread is bracketed by CUDA events on its stream; ht_timing_read
+ * returns (tag, ms) per launch since the last read.  tag = 100*has_conv_in +
+ * 10*blocks_in_pass + has_conv_out. */
+int ht_timing_enable(int on);
+int ht_timing_read(int *tags, float *ms, int max, int *count);
 
 /* ---- K1' / K2: training forward (stores activations) and backward -------
  * Replaces PolicyNetwork.forward/backward (nn.py:138-160) incl.

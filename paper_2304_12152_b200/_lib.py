@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "libhtb200.so")
+LIB_PATH = os.environ.get("HTB200_LIB") or os.path.join(HERE, "csrc", "libhtb200.so")
 
 HT_OK, HT_E_INVALID, HT_E_NONFINITE, HT_E_CUDA, HT_E_UNSUPPORTED = 0, 1, 2, 3, 4
 
@@ -36,6 +36,8 @@ SIGNATURES = {
                     _i64, _i, _vp],
     "ht_halftone_check": [_vp, _vp],
     "ht_last_launch_count": [_ip],
+    "ht_timing_enable": [_i],
+    "ht_timing_read": [_vp, _vp, _i, _ip],
     "ht_train_act_bytes": [_i, _i, _i, _i, _i, _i64p],
     "ht_policy_forward_train": [_vp, _i, _i, _vp, _i, _i, _i, _vp, _vp, _vp],
     "ht_policy_backward": [_vp, _i, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp],

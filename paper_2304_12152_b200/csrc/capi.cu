@@ -4,6 +4,8 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ht {
@@ -28,6 +30,36 @@ int fail(int code, const char *fmt, ...) {
 
 void count_launch(int n) { g_launches += n; }
 void reset_launches() { g_launches = 0; }
+
+struct TimedLaunch {
+  cudaEvent_t a, b;
+  int tag;
+};
+static thread_local bool g_timing = false;
+static thread_local std::vector<TimedLaunch> g_timed;
+static thread_local std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+bool timing_enabled() { return g_timing; }
+void timing_mark_begin(cudaStream_t st, int tag) {
+  if (!g_timing) return;
+  TimedLaunch t{pool_event(), pool_event(), tag};
+  cudaEventRecord(t.a, st);
+  g_timed.push_back(t);
+}
+void timing_mark_end(cudaStream_t st) {
+  if (!g_timing || g_timed.empty()) return;
+  cudaEventRecord(g_timed.back().b, st);
+}
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
 static inline uint64_t splitmix64(uint64_t &s) {
@@ -60,6 +92,32 @@ int ht_version(void) { return 100; }
 
 int ht_last_launch_count(int *count) {
   if (count) *count = ht::g_launches;
+  return HT_OK;
+}
+
+// Per-launch event timing of the fused forward's pass kernels.
+int ht_timing_enable(int on) {
+  ht::g_timing = on != 0;
+  return HT_OK;
+}
+// Copies up to `max` (tag, milliseconds) pairs recorded since the last read
+// (synchronises on the recorded events), then clears the record.
+int ht_timing_read(int *tags, float *ms, int max, int *count) {
+  int n = 0;
+  for (auto &t : ht::g_timed) {
+    if (n < max) {
+      HT_CUDA(cudaEventSynchronize(t.b));
+      float v = 0.f;
+      HT_CUDA(cudaEventElapsedTime(&v, t.a, t.b));
+      tags[n] = t.tag;
+      ms[n] = v;
+      ++n;
+    }
+    ht::g_event_pool.push_back(t.a);
+    ht::g_event_pool.push_back(t.b);
+  }
+  ht::g_timed.clear();
+  *count = n;
   return HT_OK;
 }
 

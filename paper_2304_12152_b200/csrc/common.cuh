@@ -41,6 +41,12 @@ int fail(int code, const char *fmt, ...);
 void count_launch(int n = 1);
 void reset_launches();
 
+// optional per-launch CUDA-event timing (ht_timing_*): when enabled, the
+// fused forward brackets every pass launch with events on its stream.
+bool timing_enabled();
+void timing_mark_begin(cudaStream_t st, int tag);
+void timing_mark_end(cudaStream_t st);
+
 // Offsets of the parameter tensors in the flat params() vector
 // (nn.py:118-122): conv_in, then per block conv1 / conv2, then conv_out.
 struct NetGeom {

@@ -26,8 +26,8 @@
 //   (and hi/lo weights) so its input is represented to ~fp32 accuracy.
 // * Per-layer zero padding (nn.py:50): out-of-image pixels are forced to 0 in
 //   every epilogue; out-of-image rows issue no MMAs.
-// * Roles (512 threads): warp 0 lane 0 issues all MMAs; warps 4-7 load the
-//   pass input rows; warps 8-15 are the epilogue (TMEM -> registers -> bias,
+// * Roles (544 threads): warp 0 lane 0 issues all MMAs; warps 1-16 are the
+//   epilogue in two sets (even / odd layers); set 0 also loads the pass input rows (TMEM -> registers -> bias,
 //   ReLU, fp16 -> next layer's shared-memory row / global x / p,h).
 //   Producer/consumer hand-offs use mbarriers; tcgen05.commit signals MMA
 //   completion.
@@ -91,6 +91,29 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
+#ifdef HT_TRACE
+#define TRACE(...) do { if (blockIdx.x == 0) printf(__VA_ARGS__); } while (0)
+#else
+#define TRACE(...) do {} while (0)
+#endif
+#ifdef HT_WATCHDOG
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (long long it = 0; !ok; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    if (it == (1ll << 22)) {
+      uint32_t base;
+      asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(base));
+      extern __shared__ __align__(1024) uint8_t smem[];
+      printf("WATCHDOG block %d thread %d bar_off %u parity %u (smem %u)\n", blockIdx.x, threadIdx.x,
+             bar - (uint32_t)__cvta_generic_to_shared(smem), parity, base);
+      asm volatile("trap;");
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -102,6 +125,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -134,7 +158,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 __host__ __device__ constexpr uint32_t idesc_f16(int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -152,7 +176,7 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   return __uint_as_float(r);
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
           taddr),
@@ -162,6 +186,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
       "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
       "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(0u)
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -180,19 +210,23 @@ struct TcParams {
   const uint8_t *w;     // this pass's weight tiles (same byte image as smem)
   const float *bias;    // G x 32 fp32
   const float *c, *z;   // HI: (B, rows, W) fp32 planes
-  const float *x_in;    // !HI: (rows, VW, 32) fp32
-  float *x_out;         // !HO: (rows, VW, 32) fp32
+  const float *x_in;    // !HI: (rows, 8, VW, 4) fp32 (channel-group planar)
+  float *x_out;         // !HO: (rows, 8, VW, 4) fp32
   float *p;             // HO: (B, out_rows, W) (nullable)
   uint8_t *h;           // HO: (B, out_rows, W) (nullable)
   int *flag;            // HO: non-finite logit flag
   int B, W, VW, rows;   // rows = window rows held by the pass buffers
   int S, n_strips;      // strip stride (valid lanes) and count
-  int band_h, n_bands, r_lo, r_hi;  // bands tile output rows [r_lo, r_hi)
+  int r_lo, r_hi;       // output rows [r_lo, r_hi) of this pass (window-relative)
+  long long chunk;      // strip-rows per CTA: CTA i owns [i*chunk, (i+1)*chunk) of
+                        // the strip-major (strip, row) space, split into segments
   int out_rows;         // HO: rows of p/h (== r_hi - r_lo)
 };
 
+constexpr int NTHREADS = 544;  // warp 0: MMA issuer | warps 1-16: epilogue (2 sets of 8)
+
 template <bool HI, int NBK, bool HO>
-__global__ void __launch_bounds__(512, 1) tc_pass_kernel(const __grid_constant__ TcParams P) {
+__global__ void __launch_bounds__(NTHREADS, 1) tc_pass_kernel(const __grid_constant__ TcParams P) {
   using PL = Plan<HI, NBK, HO>;
   constexpr int G = PL::G;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -208,7 +242,7 @@ __global__ void __launch_bounds__(512, 1) tc_pass_kernel(const __grid_constant__
   // ---- setup: barriers, zeroed row buffers, weights, biases, TMEM ----------
   if (tid == 0) {
     for (int j = 0; j < G; ++j) {
-      const uint32_t prod = (j == 0) ? 4u : 8u;  // loader warps / epilogue warps
+      const uint32_t prod = 8u;  // one epilogue set (set 0 also loads layer 0's rows)
       mbar_init(a_full(j, 0), prod);
       mbar_init(a_full(j, 1), prod);
       mbar_init(a_empty(j, 0), 1);
@@ -221,11 +255,11 @@ __global__ void __launch_bounds__(512, 1) tc_pass_kernel(const __grid_constant__
   {
     const uint4 zero = make_uint4(0, 0, 0, 0);
     uint4 *ab = reinterpret_cast<uint4 *>(smem + PL::W_TOTAL);
-    for (int i = tid; i < (PL::A_END - PL::W_TOTAL) / 16; i += 512) ab[i] = zero;
+    for (int i = tid; i < (PL::A_END - PL::W_TOTAL) / 16; i += NTHREADS) ab[i] = zero;
     const uint4 *wg = reinterpret_cast<const uint4 *>(P.w);
     uint4 *ws = reinterpret_cast<uint4 *>(smem);
-    for (int i = tid; i < PL::W_TOTAL / 16; i += 512) ws[i] = __ldg(wg + i);
-    for (int i = tid; i < G * 32; i += 512) bias_s[i] = __ldg(P.bias + i);
+    for (int i = tid; i < PL::W_TOTAL / 16; i += NTHREADS) ws[i] = __ldg(wg + i);
+    for (int i = tid; i < G * 32; i += NTHREADS) bias_s[i] = __ldg(P.bias + i);
   }
   fence_proxy_async();
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + PL::TMEMP_OFF);
@@ -238,26 +272,32 @@ __global__ void __launch_bounds__(512, 1) tc_pass_kernel(const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int n_units = P.n_strips * P.n_bands;
-  // unit geometry (identical in every role)
-  auto unit_geom = [&](int u, int &v0, int &A, int &Bn, int &R0, int &R1) {
-    const int s = u % P.n_strips, k = u / P.n_strips;
+  // Balanced work split: this CTA owns strip-rows [q0, q1) of the strip-major
+  // (strip, output row) space; it walks them as one segment per strip touched.
+  const long long range = P.r_hi - P.r_lo;
+  const long long q0 = (long long)blockIdx.x * P.chunk;
+  const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * range);
+  // segment geometry at position q (identical in every role); returns the
+  // position after the segment
+  auto seg_geom = [&](long long q, int &v0, int &A, int &Bn, int &R0, int &R1) -> long long {
+    const int s = (int)(q / range);
+    const long long end = min(q1, (long long)(s + 1) * range);
     v0 = s * P.S - G;
-    R0 = P.r_lo + k * P.band_h;
-    R1 = min(R0 + P.band_h, P.r_hi);
+    R0 = P.r_lo + (int)(q - (long long)s * range);
+    R1 = P.r_lo + (int)(end - (long long)s * range);
     A = max(R0 - G, 0);
     Bn = min(R1 + G, P.rows);
+    return end;
   };
 
   if (warp == 0) {
     // ===================== MMA issuer (one thread) ============================
     if (lane == 0) {
       uint32_t ph_afull = 0, ph_free = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (long long q = q0; q < q1;) {
         int v0, A, Bn, R0, R1;
-        unit_geom(u, v0, A, Bn, R0, R1);
-        if (R0 >= R1) continue;
-        for (int t = A; t <= Bn + 2 * (G - 1); ++t) {
+        q = seg_geom(q, v0, A, Bn, R0, R1);
+        for (int t = A; t < Bn + 2 * (G - 1); ++t) {
           rev_for<G>([&](auto JC) {
             constexpr int j = decltype(JC)::value;
             const int r = t - 2 * j;
@@ -287,217 +327,249 @@ __global__ void __launch_bounds__(512, 1) tc_pass_kernel(const __grid_constant__
               }
               tc_commit(a_empty(j, q));
               tc_commit(acc_full(j));
-            } else if (r == Bn) {
-              tc_commit(acc_full(j));
+              TRACE("MMA t=%d j=%d r=%d issued\n", t, j, r);
             }
+            // no commit on the drain-only step r == Bn: the last row's data is
+            // covered by the previous completion, and two back-to-back
+            // completions could let a slow waiter miss a parity phase
           });
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ===================== loader: pass input rows -> layer 0 A buffer ========
-    const int l = tid - 128;  // strip lane 0..127
-    uint32_t ph_empty = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int v0, A, Bn, R0, R1;
-      unit_geom(u, v0, A, Bn, R0, R1);
-      if (R0 >= R1) continue;
-      const int v = v0 + l;
-      const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
-      const bool in_img = v >= 0 && v < P.VW && col < P.W;
-      constexpr int NV = HI ? 2 : 32;
-      float cur[NV], nxt[NV];
-      auto load_row = [&](int t, float *dst) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) dst[i] = 0.f;
-        if (!in_img || t >= Bn) return;
-        if constexpr (HI) {
-          const size_t idx = ((size_t)b * P.rows + t) * P.W + col;
-          dst[0] = __ldg(P.c + idx);
-          dst[1] = __ldg(P.z + idx);
-        } else {
-          const float4 *src = reinterpret_cast<const float4 *>(P.x_in + ((size_t)t * P.VW + v) * 32);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 f = __ldg(src + i);
-            dst[4 * i] = f.x; dst[4 * i + 1] = f.y; dst[4 * i + 2] = f.z; dst[4 * i + 3] = f.w;
-          }
-        }
-      };
-      load_row(A, cur);
-      for (int t = A; t < Bn; ++t) {
-        load_row(t + 1, nxt);
-        const int q = t & 1;
-        if (t - 2 >= A) {
-          mbar_wait(a_empty(0, q), (ph_empty >> q) & 1);
-          ph_empty ^= 1u << q;
-        }
-        const uint32_t dst = sbase + PL::a_off(0) + q * PL::abytes(0) + (l + 1) * 16;
-        if constexpr (HI) {
-          // K=16 channel slots: [c_hi, c_lo, c_hi, z_hi, z_lo, z_hi, 0..]
-          const __half ch = __float2half_rn(cur[0]);
-          const __half cl = __float2half_rn(cur[0] - __half2float(ch));
-          const __half zh = __float2half_rn(cur[1]);
-          const __half zl = __float2half_rn(cur[1] - __half2float(zh));
-          __half2 p0 = __halves2half2(ch, cl), p1 = __halves2half2(ch, zh), p2 = __halves2half2(zl, zh);
-          st_shared_v4(dst, *reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1),
-                       *reinterpret_cast<uint32_t *>(&p2), 0u);
-        } else {
-#pragma unroll
-          for (int cch = 0; cch < 4; ++cch)
-            st_shared_v4(dst + cch * PLANE, pack_h2(cur[8 * cch], cur[8 * cch + 1]),
-                         pack_h2(cur[8 * cch + 2], cur[8 * cch + 3]), pack_h2(cur[8 * cch + 4], cur[8 * cch + 5]),
-                         pack_h2(cur[8 * cch + 6], cur[8 * cch + 7]));
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(a_full(0, q));
-#pragma unroll
-        for (int i = 0; i < NV; ++i) cur[i] = nxt[i];
-      }
-      for (int t = max(A, Bn - 2); t < Bn; ++t) {
-        const int q = t & 1;
-        mbar_wait(a_empty(0, q), (ph_empty >> q) & 1);
-        ph_empty ^= 1u << q;
-      }
-    }
-  } else if (warp >= 8) {
-    // ===================== epilogue ===========================================
-    const int ew = warp - 8, quarter = warp & 3, hf = ew >> 2;
+  } else {
+    // ===================== epilogue: two warp sets ============================
+    // Set s handles the layers j with j % 2 == s (a conv2 and the layer that
+    // holds its residual are two layers apart, so they share a set and the fp32
+    // residual rows stay in the same thread's registers).  Within a set the 8
+    // warps cover the 4 TMEM lane quarters x 2 channel halves.  Set 0 also
+    // streams the pass input rows into layer 0's A buffer, one row ahead, with
+    // the global loads prefetched a further row ahead in registers.
+    const int ew = (warp - 1) & 7;
+    const int quarter = warp & 3, hf = ew >> 2;
     const int l = quarter * 32 + lane;
     const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16);
-    uint32_t ph_full = 0, ph_empty = 0;
-    float held[2][16];
-    float pre[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) { held[0][i] = held[1][i] = pre[i] = 0.f; }
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int v0, A, Bn, R0, R1;
-      unit_geom(u, v0, A, Bn, R0, R1);
-      if (R0 >= R1) continue;
-      const int v = v0 + l;
-      const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
-      const bool in_img = v >= 0 && v < P.VW && col < P.W;
-      const bool lane_valid = l >= G && l < G + P.S && v >= 0 && v < P.VW;
-      auto load_resid = [&](int e) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pre[i] = 0.f;
+    // one code path per set: the compiler then only keeps that set's
+    // register arrays live (held / pre for conv2 residuals, pf for loads)
+    auto epilogue = [&](auto SETC) {
+      constexpr int set = decltype(SETC)::value;
+      uint32_t ph_full = 0, ph_empty = 0, ph_in = 0;
+      float held[2][16];
+      float pre[16];
+      constexpr int NV = HI ? 2 : 16;
+      float pf[NV];
+  #pragma unroll
+      for (int i = 0; i < 16; ++i) { held[0][i] = held[1][i] = pre[i] = 0.f; }
+      for (long long qq = q0; qq < q1;) {
+        int v0, A, Bn, R0, R1;
+        qq = seg_geom(qq, v0, A, Bn, R0, R1);
+        const int v = v0 + l;
+        const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
+        const bool in_img = v >= 0 && v < P.VW && col < P.W;
+        const bool lane_valid = l >= G && l < G + P.S && v >= 0 && v < P.VW;
+        // pass buffers are channel-group planar: [row][group of 4 channels][v][4]
+        // (float4 index), so a warp's 16-byte accesses are 512 contiguous bytes
+        auto xoff = [&](int row, int g) { return ((size_t)row * 8 + g) * P.VW + v; };
+        auto load_resid = [&](int e) {
+  #pragma unroll
+          for (int i = 0; i < 16; ++i) pre[i] = 0.f;
+          if constexpr (!HI) {
+            if (e < Bn && v >= 0 && v < P.VW) {
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(e, 4 * hf + i));
+                pre[4 * i] = f.x; pre[4 * i + 1] = f.y; pre[4 * i + 2] = f.z; pre[4 * i + 3] = f.w;
+              }
+            }
+          }
+        };
         if constexpr (!HI) {
-          if (e < Bn && v >= 0 && v < P.VW) {
-            const float4 *src = reinterpret_cast<const float4 *>(P.x_in + ((size_t)e * P.VW + v) * 32 + hf * 16);
-#pragma unroll
+          if (set == 1) load_resid(A);   // layer 1 (a conv2) takes its residual from the pass input
+        }
+        // pass input row t -> registers (set 0): (c, z) or 16 channels of x
+        auto load_in = [&](int t) {
+  #pragma unroll
+          for (int i = 0; i < NV; ++i) pf[i] = 0.f;
+          if (!in_img || t >= Bn) return;
+          if constexpr (HI) {
+            const size_t idx = ((size_t)b * P.rows + t) * P.W + col;
+            pf[0] = __ldg(P.c + idx);
+            pf[1] = __ldg(P.z + idx);
+          } else {
+  #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float4 f = __ldg(src + i);
-              pre[4 * i] = f.x; pre[4 * i + 1] = f.y; pre[4 * i + 2] = f.z; pre[4 * i + 3] = f.w;
+              const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(t, 4 * hf + i));
+              pf[4 * i] = f.x; pf[4 * i + 1] = f.y; pf[4 * i + 2] = f.z; pf[4 * i + 3] = f.w;
             }
           }
-        }
-      };
-      if constexpr (!HI) load_resid(A);
-      for (int t = A - 2; t <= Bn + 2 * (G - 1); ++t) {
-        rev_for<G>([&](auto JC) {
-          constexpr int j = decltype(JC)::value;
-          constexpr int kind = PL::kind(j), ns = PL::ns(j);
-          const int r = t - 2 * j;
-          if (r >= A && r <= Bn) {
-            mbar_wait(acc_full(j), (ph_full >> j) & 1);
-            ph_full ^= 1u << j;
-            tc_fence_after();
-          }
-          // ---- drain output row d = r - 1 ----
-          const int d = r - 1;
-          if (d >= A && d < Bn) {
-            const uint32_t taddr = tlane + PL::tcol(j) + (d % 3) * ns;
-            if constexpr (kind == K_OUT) {
-              if (hf == 0) {
-                const float logit = tmem_ld1(taddr) + bias_s[j * 32];
-                if (lane_valid && in_img && d >= R0 && d < R1) {
-                  if (!isfinite(logit)) atomicOr(P.flag, 1);
-                  const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
-                  if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
-                  if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
-                }
-              }
-            } else {
-              float val[16];
-              tmem_ld16(taddr + hf * 16, val);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                float x = val[i];
-                if constexpr (kind == K_IN) x += bias_s[j * 32 + hf * 16 + i];
-                if constexpr (kind == K_C1) x = fmaxf(x + bias_s[j * 32 + hf * 16 + i], 0.f);
-                val[i] = in_img ? x : 0.f;
-              }
-              if constexpr (PL::holds(j)) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) held[PL::hold_idx(j)][i] = val[i];
-              }
-              if constexpr (PL::feeds_next(j)) {
-                const int q = d & 1;
-                if (d - 2 >= A) {
-                  mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
-                  ph_empty ^= 1u << (2 * (j + 1) + q);
-                }
-                const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16 +
-                                     (2 * hf) * PLANE;
-                st_shared_v4(dst, pack_h2(val[0], val[1]), pack_h2(val[2], val[3]), pack_h2(val[4], val[5]),
-                             pack_h2(val[6], val[7]));
-                st_shared_v4(dst + PLANE, pack_h2(val[8], val[9]), pack_h2(val[10], val[11]),
-                             pack_h2(val[12], val[13]), pack_h2(val[14], val[15]));
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(a_full(j + 1, q));
-              } else {
-                // last layer of a non-output pass: fp32 x -> global
-                if (lane_valid && d >= R0 && d < R1) {
-                  float4 *dstg = reinterpret_cast<float4 *>(P.x_out + ((size_t)d * P.VW + v) * 32 + hf * 16);
-#pragma unroll
-                  for (int i = 0; i < 4; ++i)
-                    dstg[i] = make_float4(val[4 * i], val[4 * i + 1], val[4 * i + 2], val[4 * i + 3]);
-                }
-              }
-            }
-          }
-          // ---- init accumulator slot for row e = r + 2 ----
-          const int e = r + 2;
-          if (e >= A && e < Bn) {
-            const uint32_t taddr = tlane + PL::tcol(j) + (e % 3) * ns;
-            float init[16];
-            if constexpr (kind == K_C2) {
-              if constexpr (j >= 2 && PL::holds(j >= 2 ? j - 2 : 0)) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                  init[i] = held[PL::hold_idx(j - 2)][i] + bias_s[j * 32 + hf * 16 + i];
-              } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) init[i] = pre[i] + bias_s[j * 32 + hf * 16 + i];
-                load_resid(e + 1);
-              }
-              tmem_st16(taddr + hf * 16, init);
-            } else if (kind != K_OUT || hf == 0) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) init[i] = 0.f;
-              tmem_st16(taddr + (kind == K_OUT ? 0 : hf * 16), init);
-            }
-          }
-          if (r + 1 >= A && r + 1 < Bn) {
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_free(j));
-          }
-        });
-      }
-      // consume the trailing a_empty completions of the buffers we produce into
-#pragma unroll
-      for (int j = 0; j + 1 < G; ++j) {
-        for (int t = max(A, Bn - 2); t < Bn; ++t) {
+        };
+        // registers (row t) -> layer 0's A buffer, then prefetch row t+1
+        auto store_in = [&](int t) {
           const int q = t & 1;
-          mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
-          ph_empty ^= 1u << (2 * (j + 1) + q);
+          if (t - 2 >= A) {
+            if (lane == 0) mbar_wait(a_empty(0, q), (ph_in >> q) & 1);
+            ph_in ^= 1u << q;
+            __syncwarp();
+          }
+          const uint32_t dst = sbase + PL::a_off(0) + q * PL::abytes(0) + (l + 1) * 16;
+          if constexpr (HI) {
+            if (hf == 0) {
+              // K=16 channel slots: [c_hi, c_lo, c_hi, z_hi, z_lo, z_hi, 0, 0 | 0 x 8]
+              const __half ch = __float2half_rn(pf[0]);
+              const __half cl = __float2half_rn(pf[0] - __half2float(ch));
+              const __half zh = __float2half_rn(pf[1]);
+              const __half zl = __float2half_rn(pf[1] - __half2float(zh));
+              __half2 p0 = __halves2half2(ch, cl), p1 = __halves2half2(ch, zh), p2 = __halves2half2(zl, zh);
+              st_shared_v4(dst, *reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1),
+                           *reinterpret_cast<uint32_t *>(&p2), 0u);
+            }
+          } else {
+            const uint32_t d2 = dst + (2 * hf) * PLANE;
+            st_shared_v4(d2, pack_h2(pf[0], pf[1]), pack_h2(pf[2], pf[3]), pack_h2(pf[4], pf[5]),
+                         pack_h2(pf[6], pf[7]));
+            st_shared_v4(d2 + PLANE, pack_h2(pf[8], pf[9]), pack_h2(pf[10], pf[11]), pack_h2(pf[12], pf[13]),
+                         pack_h2(pf[14], pf[15]));
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full(0, q));
+          if (lane == 0) TRACE("LOAD warp %d stored row %d\n", warp, t);
+          load_in(t + 1);
+        };
+        if (set == 0) load_in(A);
+        for (int t = A - 2; t <= Bn + 2 * (G - 1); ++t) {
+          rev_for<G>([&](auto JC) {
+            constexpr int j = decltype(JC)::value;
+            if constexpr ((j & 1) != set) return;
+            else {
+            constexpr int kind = PL::kind(j), ns = PL::ns(j);
+            const int r = t - 2 * j;
+            if (r >= A && r < Bn) {
+              if (lane == 0) mbar_wait(acc_full(j), (ph_full >> j) & 1);
+              if (lane == 0) TRACE("EPI warp %d t=%d j=%d acc_full ok\n", warp, t, j);
+              ph_full ^= 1u << j;
+              __syncwarp();
+              tc_fence_after();
+            }
+            const int d = r - 1, e = r + 2;
+            const bool do_drain = d >= A && d < Bn;
+            const bool do_init = e >= A && e < Bn;
+            // ---- 1. load the finished row d from TMEM ----
+            float val[16];
+            float logit = 0.f;
+            if (do_drain) {
+              const uint32_t taddr = tlane + PL::tcol(j) + (d % 3) * ns;
+              if constexpr (kind == K_OUT) {
+                if (hf == 0) logit = tmem_ld1(taddr);
+              } else {
+                tmem_ld16(taddr + hf * 16, val);
+              }
+            }
+            // ---- 2. initialise slot of row e (same slot as d: after the load) and
+            //         release the MMA for this layer's next row ----
+            if (do_init) {
+              // in place: the held / prefetched residual row is consumed exactly once
+              const uint32_t taddr = tlane + PL::tcol(j) + (e % 3) * ns;
+              if constexpr (kind == K_C2) {
+                if constexpr (j >= 2 && PL::holds(j >= 2 ? j - 2 : 0)) {
+                  constexpr int hi_ = PL::hold_idx(j - 2);
+  #pragma unroll
+                  for (int i = 0; i < 16; ++i) held[hi_][i] += bias_s[j * 32 + hf * 16 + i];
+                  tmem_st16(taddr + hf * 16, held[hi_]);
+                } else {
+  #pragma unroll
+                  for (int i = 0; i < 16; ++i) pre[i] += bias_s[j * 32 + hf * 16 + i];
+                  tmem_st16(taddr + hf * 16, pre);
+                }
+              } else if (kind != K_OUT || hf == 0) {
+                tmem_st16_zero(taddr + (kind == K_OUT ? 0 : hf * 16));
+              }
+            }
+            if (r + 1 >= A && r + 1 < Bn) {
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acc_free(j));
+            }
+            if constexpr (kind == K_C2 && !(j >= 2 && PL::holds(j >= 2 ? j - 2 : 0))) {
+              if (do_init) load_resid(e + 1);
+            }
+            // ---- 3. epilogue math + hand-off of row d ----
+            if (do_drain) {
+              if constexpr (kind == K_OUT) {
+                if (hf == 0) {
+                  logit += bias_s[j * 32];
+                  if (lane_valid && in_img && d >= R0 && d < R1) {
+                    if (!isfinite(logit)) atomicOr(P.flag, 1);
+                    const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
+                    if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
+                    if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
+                  }
+                }
+              } else {
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  float x = val[i];
+                  if constexpr (kind == K_IN) x += bias_s[j * 32 + hf * 16 + i];
+                  if constexpr (kind == K_C1) x = fmaxf(x + bias_s[j * 32 + hf * 16 + i], 0.f);
+                  val[i] = in_img ? x : 0.f;
+                }
+                if constexpr (PL::holds(j)) {
+  #pragma unroll
+                  for (int i = 0; i < 16; ++i) held[PL::hold_idx(j)][i] = val[i];
+                }
+                if constexpr (PL::feeds_next(j)) {
+                  const int q = d & 1;
+                  if (d - 2 >= A) {
+                    if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
+                    ph_empty ^= 1u << (2 * (j + 1) + q);
+                    __syncwarp();
+                  }
+                  const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16 +
+                                       (2 * hf) * PLANE;
+                  st_shared_v4(dst, pack_h2(val[0], val[1]), pack_h2(val[2], val[3]), pack_h2(val[4], val[5]),
+                               pack_h2(val[6], val[7]));
+                  st_shared_v4(dst + PLANE, pack_h2(val[8], val[9]), pack_h2(val[10], val[11]),
+                               pack_h2(val[12], val[13]), pack_h2(val[14], val[15]));
+                  fence_proxy_async();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(a_full(j + 1, q));
+                } else {
+                  // last layer of a non-output pass: fp32 x -> global
+                  if (lane_valid && d >= R0 && d < R1) {
+                    float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
+  #pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                      dstg[xoff(d, 4 * hf + i)] = make_float4(val[4 * i], val[4 * i + 1], val[4 * i + 2], val[4 * i + 3]);
+                  }
+                }
+              }
+            }
+            }  // layer of this set
+          });
+          if (set == 0 && t + 1 >= A && t + 1 < Bn) store_in(t + 1);
         }
+        // consume the trailing a_empty completions of the buffers we produce into
+  #pragma unroll
+        for (int j = 0; j + 1 < G; ++j) {
+          if ((j & 1) != set) continue;
+          for (int t = max(A, Bn - 2); t < Bn; ++t) {
+            const int q = t & 1;
+            if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
+            ph_empty ^= 1u << (2 * (j + 1) + q);
+          }
+        }
+        if (set == 0) {
+          for (int t = max(A, Bn - 2); t < Bn; ++t) {
+            const int q = t & 1;
+            if (lane == 0) mbar_wait(a_empty(0, q), (ph_in >> q) & 1);
+            ph_in ^= 1u << q;
+          }
+        }
+        __syncwarp();
       }
-    }
+    };
+    if (((warp - 1) >> 3) == 0) epilogue(std::integral_constant<int, 0>{});
+    else epilogue(std::integral_constant<int, 1>{});
   }
   tc_fence_before();
   __syncthreads();
@@ -590,7 +662,7 @@ struct PassDesc {
 };
 
 template <bool HI, int NBK, bool HO>
-static int launch_pass(const TcParams &prm, int n_units, int n_sm, cudaStream_t st) {
+static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
   using PL = Plan<HI, NBK, HO>;
   static_assert(PL::TCOLS <= 512, "TMEM columns exceeded");
   static_assert(PL::SMEM <= 232448, "shared memory exceeded");
@@ -600,8 +672,9 @@ static int launch_pass(const TcParams &prm, int n_units, int n_sm, cudaStream_t 
     HT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM));
     attr = true;
   }
-  const int grid = n_units < n_sm ? n_units : n_sm;
-  kern<<<grid, 512, PL::SMEM, st>>>(prm);
+  timing_mark_begin(st, (HI ? 100 : 0) + NBK * 10 + (HO ? 1 : 0));
+  kern<<<grid, NTHREADS, PL::SMEM, st>>>(prm);
+  timing_mark_end(st);
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
@@ -649,22 +722,23 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     prm.r_lo = pd.ho ? out_row0 - in_row0 : 0;
     prm.r_hi = pd.ho ? out_row0 - in_row0 + out_rows : in_rows;
     prm.out_rows = out_rows;
-    const int range = prm.r_hi - prm.r_lo;
-    int nbands = (4 * n_sm + prm.n_strips - 1) / prm.n_strips;
-    int bh = (range + nbands - 1) / nbands;
-    if (bh < 8 * G) bh = 8 * G;
-    nbands = (range + bh - 1) / bh;
-    prm.band_h = bh;
-    prm.n_bands = nbands;
-    const int units = prm.n_strips * nbands;
+    // balanced split of the strip-major (strip, row) space over the SMs; each
+    // CTA gets >= 8G rows so halo recompute stays small
+    const long long total = (long long)prm.n_strips * (prm.r_hi - prm.r_lo);
+    long long grid = n_sm;
+    if (total < grid * 8 * G) grid = (total + 8 * G - 1) / (8 * G);
+    if (grid < 1) grid = 1;
+    prm.chunk = (total + grid - 1) / grid;
+    grid = (total + prm.chunk - 1) / prm.chunk;
+    const int g = (int)grid;
     int rc;
-    if (pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<true, 2, false>(prm, units, n_sm, st);
-    else if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, units, n_sm, st);
-    else if (pd.hi && pd.nbk == 0 && !pd.ho) rc = launch_pass<true, 0, false>(prm, units, n_sm, st);
-    else if (!pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<false, 2, false>(prm, units, n_sm, st);
-    else if (!pd.hi && pd.nbk == 2 && pd.ho) rc = launch_pass<false, 2, true>(prm, units, n_sm, st);
-    else if (!pd.hi && pd.nbk == 1 && pd.ho) rc = launch_pass<false, 1, true>(prm, units, n_sm, st);
-    else if (!pd.hi && pd.nbk == 0 && pd.ho) rc = launch_pass<false, 0, true>(prm, units, n_sm, st);
+    if (pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<true, 2, false>(prm, g, st);
+    else if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, g, st);
+    else if (pd.hi && pd.nbk == 0 && !pd.ho) rc = launch_pass<true, 0, false>(prm, g, st);
+    else if (!pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<false, 2, false>(prm, g, st);
+    else if (!pd.hi && pd.nbk == 2 && pd.ho) rc = launch_pass<false, 2, true>(prm, g, st);
+    else if (!pd.hi && pd.nbk == 1 && pd.ho) rc = launch_pass<false, 1, true>(prm, g, st);
+    else if (!pd.hi && pd.nbk == 0 && pd.ho) rc = launch_pass<false, 0, true>(prm, g, st);
     else return fail(HT_E_UNSUPPORTED, "no kernel for pass (hi=%d nbk=%d ho=%d)", pd.hi, pd.nbk, pd.ho);
     if (rc) return rc;
     in_x = out_x;

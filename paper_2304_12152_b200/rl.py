@@ -267,3 +267,84 @@ def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None):
             on_iteration(t, diag, net, adam, rng)
     adam.pull_state()
     return net, adam, rng
+
+
+# ---------------------------------------------------------------------------
+# batched end-to-end engine (host buffers in, halftones out)
+
+class HalftoneEngine:
+    """Reusable batched halftoner for a fixed (B, H, W): host contone/noise
+    (float32, ideally pinned) in, uint8 halftones (1 = white) or PBM P4
+    payloads out.  The batch is split into `chunks` groups of images that
+    flow through H2D -> fused K1 kernel -> D2H on alternating CUDA streams, so
+    copies of one chunk overlap the kernel of another.  Every call performs
+    the full host->device->host round trip."""
+
+    def __init__(self, net, B, H, W, chunks=4, output="h", impl=None):
+        torch = _torch()
+        _lib.require_cuda()
+        if output not in ("h", "pbm", "p"):
+            raise ValueError("output must be 'h', 'pbm' or 'p'")
+        self.net, self.B, self.H, self.W = net, B, H, W
+        self.output = output
+        self.impl = impl
+        chunks = max(1, min(chunks, B))
+        bounds = np.linspace(0, B, chunks + 1).round().astype(int)
+        self.groups = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        dev = net.device
+        self.dev = dev
+        self.streams = [torch.cuda.Stream(dev) for _ in range(2)]
+        self.c = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        self.z = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        if output == "pbm":
+            self.out = torch.empty((B, H, (W + 7) // 8), dtype=torch.uint8, device=dev)
+        elif output == "h":
+            self.out = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+        else:
+            self.out = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        self.ws = [None, None]
+        net.sync()
+
+    def out_shape(self):
+        return tuple(self.out.shape)
+
+    def h2d_bytes(self):
+        return 2 * self.B * self.H * self.W * 4
+
+    def d2h_bytes(self):
+        return self.out.numel() * self.out.element_size()
+
+    def __call__(self, c_host, z_host, out_host):
+        """c_host, z_host: (B,H,W) float32 CPU tensors (pinned for async
+        copies); out_host: CPU tensor shaped out_shape()."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.dev)
+        for k, (a, b) in enumerate(self.groups):
+            s = self.streams[k % 2]
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                self.c[a:b].copy_(c_host[a:b], non_blocking=True)
+                self.z[a:b].copy_(z_host[a:b], non_blocking=True)
+                kw = {"h_out" if self.output == "h" else
+                      ("pbm_out" if self.output == "pbm" else "p_out"): self.out[a:b]}
+                self.ws[k % 2] = self.net.halftone_device(
+                    self.c[a:b], self.z[a:b], impl=self.impl, workspace=self.ws[k % 2],
+                    stream=s, **kw)
+                out_host[a:b].copy_(self.out[a:b], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        cur.synchronize()
+        return out_host
+
+
+def halftone_batch(net, contones, noises, output="h", chunks=4):
+    """Batched public entry: (B,H,W) contones + noise maps (numpy or CPU
+    tensors) -> uint8 halftones (1 = white) or PBM payloads (numpy)."""
+    torch = _torch()
+    c = torch.as_tensor(np.ascontiguousarray(contones, dtype=np.float32)).pin_memory()
+    z = torch.as_tensor(np.ascontiguousarray(noises, dtype=np.float32)).pin_memory()
+    if c.dim() == 2:
+        c, z = c[None], z[None]
+    eng = HalftoneEngine(net, *c.shape, chunks=chunks, output=output)
+    out = torch.empty(eng.out_shape(), dtype=eng.out.dtype).pin_memory()
+    return eng(c, z, out).numpy()

@@ -155,3 +155,17 @@ def test_device_api_without_sync_reuses_packed_weights():
     net.conv_out.bias.value[0] += 1.0
     _, p2 = rl.halftone(net, c, z)
     assert np.all(p2 > p1)
+
+
+@pytest.mark.parametrize("nb", [0, 1, 2, 3, 5])
+def test_fused_pass_plans_for_other_depths(nb):
+    """Every pass-plan shape of the fused kernel (conv_in-only, conv_out-only,
+    odd block counts) against the fp32 SIMT path on the same net."""
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05, 32, nb, seed=nb)
+    c = synth.contone(45, 300, seed=nb)
+    z = gaussian_noise_map_f32(Rng(nb), 300, 45)
+    h0, p0 = rl.halftone(net, c, z, impl=0)
+    h1, p1 = rl.halftone(net, c, z, impl=1)
+    _check(p0, h0, p1, P_TOL)
