@@ -66,21 +66,21 @@ struct Plan {
   static constexpr int W_TOTAL = w_off(G - 1) + wbytes(G - 1);
   static constexpr int a_off(int j) { return j == 0 ? W_TOTAL : a_off(j - 1) + 2 * abytes(j - 1); }
   static constexpr int A_END = a_off(G - 1) + 2 * abytes(G - 1);
-  static constexpr int BIAS_OFF = A_END;                       // G*32 fp32
-  static constexpr int BAR_OFF = BIAS_OFF + G * 32 * 4;        // barriers (8 B each)
-  // barriers: a_full[G][2], a_empty[G][2], acc_full[G], acc_free[G]
-  static constexpr int NBAR = 6 * G;
+  // barriers: a_full[G][2], a_empty[G][2], acc_full[G], link_full[2], link_empty[2]
+  static constexpr int BAR_OFF = A_END;
+  static constexpr int NBAR = 5 * G + 4;
   static constexpr int TMEMP_OFF = BAR_OFF + NBAR * 8;
   static constexpr int SMEM = TMEMP_OFF + 16;
   static constexpr int tcol(int j) { return j == 0 ? 0 : tcol(j - 1) + 3 * ns(j - 1); }
-  static constexpr int TCOLS = tcol(G - 1) + 3 * ns(G - 1);
-  // layer j writes its output into the next layer's A buffer
+  static constexpr int LINK_COL = tcol(G - 1) + 3 * ns(G - 1);   // residual link: 2 rows x 32 fp32
+  static constexpr int TCOLS = LINK_COL + 64;
   static constexpr bool feeds_next(int j) { return j < G - 1; }
-  // layer j's output is the residual of layer j+2 (a conv2)
+  // layer j's output is the residual of layer j+2 (a conv2) -> written to the TMEM link
   static constexpr bool holds(int j) {
     return (kind(j) == K_IN || kind(j) == K_C2) && j + 2 < G && kind(j + 2) == K_C2;
   }
-  static constexpr int hold_idx(int j) { return j <= 0 ? 0 : hold_idx(j - 1) + (holds(j - 1) ? 1 : 0); }
+  // a conv2 whose residual comes from the pass input (global) instead of the link
+  static constexpr bool global_resid(int j) { return kind(j) == K_C2 && !(j >= 2 && holds(j - 2)); }
 };
 
 // ---------------------------------------------------------------------------
@@ -91,6 +91,28 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
+#ifdef HT_TIMELINE
+// debug timeline of CTA 0: per-role private slots (no atomics), (ev, t, j, clock)
+__device__ long long g_tl[4][4 * 16384];
+#define TL_DECL int tl_n_ = 0;
+#define TL(role, ev, t, j) do { if (blockIdx.x == 0 && tl_n_ < 16384) { long long *p_ = &g_tl[role][4 * tl_n_++]; \
+  p_[0] = (ev); p_[1] = (t); p_[2] = (j); p_[3] = clock64(); } } while (0)
+#else
+#define TL_DECL
+#define TL(role, ev, t, j) do {} while (0)
+#endif
+#ifdef HT_PROF
+// per (group, warp-in-group 0/1) cycle accumulators of CTA 0, lane 0
+__device__ long long g_prof[8][16];
+#define PROF_DECL long long pacc_[16] = {0}; long long pt_ = clock64();
+#define PROF_MARK(k) do { long long n_ = clock64(); pacc_[k] += n_ - pt_; pt_ = n_; } while (0)
+#define PROF_DUMP(slot) do { if (blockIdx.x == 0 && lane == 0 && (slot) < 8) \
+  for (int k_ = 0; k_ < 16; ++k_) g_prof[slot][k_] = pacc_[k_]; } while (0)
+#else
+#define PROF_DECL
+#define PROF_MARK(k) do {} while (0)
+#define PROF_DUMP(set) do {} while (0)
+#endif
 #ifdef HT_TRACE
 #define TRACE(...) do { if (blockIdx.x == 0) printf(__VA_ARGS__); } while (0)
 #else
@@ -114,11 +136,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 #else
+// try_wait with a suspend-time hint: a blocked warp sleeps until the phase
+// completes instead of spinning and stealing issue slots from working warps
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n"
       "DONE_%=:\n\t}" ::"r"(bar),
@@ -147,6 +171,15 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1));
+}
+// one elected lane of a converged warp issues the MMA (keeps operands uniform)
+__device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1));
 }
 // UMMA shared-memory descriptor: K-major, no swizzle, version 1 (sm_100)
@@ -208,7 +241,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 // ---------------------------------------------------------------------------
 struct TcParams {
   const uint8_t *w;     // this pass's weight tiles (same byte image as smem)
-  const float *bias;    // G x 32 fp32
+  int layer0;           // index of the pass's first layer in c_bias
   const float *c, *z;   // HI: (B, rows, W) fp32 planes
   const float *x_in;    // !HI: (rows, 8, VW, 4) fp32 (channel-group planar)
   float *x_out;         // !HO: (rows, 8, VW, 4) fp32
@@ -223,43 +256,104 @@ struct TcParams {
   int out_rows;         // HO: rows of p/h (== r_hi - r_lo)
 };
 
-constexpr int NTHREADS = 544;  // warp 0: MMA issuer | warps 1-16: epilogue (2 sets of 8)
+// Biases live in the constant bank (not SMEM: the tensor core's operand reads
+// saturate shared-memory bandwidth and starve LSU loads).  Filled per
+// ht_halftone call with a stream-ordered device->constant copy.
+constexpr int MAX_BIAS = 64 * 32;
+__constant__ float c_bias[MAX_BIAS];
+#define PBIAS(j, i) c_bias[(P.layer0 + (j)) * 32 + (i)]
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])),
+      "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
+      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])),
+      "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One 4-warp group per layer (128 threads = the 128 pixel lanes of a strip
+// row; warp k of a group owns TMEM lane quarter k; each thread owns one pixel
+// and all 32 channels).  Per step t a group, for its layer j and input row
+// r = t - 2j:
+//   1. waits for MMA(r) to complete (acc_full)
+//   2. loads the finished output row d = r-1 from its TMEM slot
+//   3. re-initialises that slot for row e = r+2 (bias, or residual + bias;
+//      the residual comes from the pass input or from the TMEM link)
+//   4. (layer 0 only) stores pass-input row r+1 into its A buffer
+//   5. hands row d on: activation, link write, fp16 row for the next layer
+//      (or fp32 x to global / p,h for the output layer)
+//   6. group barrier, then one elected thread issues MMA(r+1) (6 UMMAs) once
+//      the previous layer has handed row r+1 over (a_full).
+// A layer's MMA for step t+1 depends on the previous layer's hand-off from
+// step t only, so layers run concurrently and the tensor pipe is shared.
 template <bool HI, int NBK, bool HO>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_pass_kernel(const __grid_constant__ TcParams P) {
+__global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(const __grid_constant__ TcParams P) {
   using PL = Plan<HI, NBK, HO>;
   constexpr int G = PL::G;
+  constexpr int NT = 128 * G;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + PL::BAR_OFF;
   auto a_full = [&](int j, int q) { return bar0 + 8u * (j * 2 + q); };
   auto a_empty = [&](int j, int q) { return bar0 + 8u * (2 * G + j * 2 + q); };
   auto acc_full = [&](int j) { return bar0 + 8u * (4 * G + j); };
-  auto acc_free = [&](int j) { return bar0 + 8u * (5 * G + j); };
-  float *bias_s = reinterpret_cast<float *>(smem + PL::BIAS_OFF);
+  auto link_full = [&](int q) { return bar0 + 8u * (5 * G + q); };
+  auto link_empty = [&](int q) { return bar0 + 8u * (5 * G + 2 + q); };
 
-  // ---- setup: barriers, zeroed row buffers, weights, biases, TMEM ----------
+  // ---- setup: barriers, zeroed row buffers, weights, TMEM --------------------
   if (tid == 0) {
     for (int j = 0; j < G; ++j) {
-      const uint32_t prod = 8u;  // one epilogue set (set 0 also loads layer 0's rows)
-      mbar_init(a_full(j, 0), prod);
-      mbar_init(a_full(j, 1), prod);
-      mbar_init(a_empty(j, 0), 1);
+      mbar_init(a_full(j, 0), 4);   // the producing group's 4 warps
+      mbar_init(a_full(j, 1), 4);
+      mbar_init(a_empty(j, 0), 1);  // tcgen05.commit
       mbar_init(a_empty(j, 1), 1);
       mbar_init(acc_full(j), 1);
-      mbar_init(acc_free(j), 8);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(link_full(q), 4);
+      mbar_init(link_empty(q), 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   {
     const uint4 zero = make_uint4(0, 0, 0, 0);
     uint4 *ab = reinterpret_cast<uint4 *>(smem + PL::W_TOTAL);
-    for (int i = tid; i < (PL::A_END - PL::W_TOTAL) / 16; i += NTHREADS) ab[i] = zero;
+    for (int i = tid; i < (PL::A_END - PL::W_TOTAL) / 16; i += NT) ab[i] = zero;
     const uint4 *wg = reinterpret_cast<const uint4 *>(P.w);
     uint4 *ws = reinterpret_cast<uint4 *>(smem);
-    for (int i = tid; i < PL::W_TOTAL / 16; i += NTHREADS) ws[i] = __ldg(wg + i);
-    for (int i = tid; i < G * 32; i += NTHREADS) bias_s[i] = __ldg(P.bias + i);
+    for (int i = tid; i < PL::W_TOTAL / 16; i += NT) ws[i] = __ldg(wg + i);
   }
   fence_proxy_async();
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + PL::TMEMP_OFF);
@@ -270,15 +364,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_pass_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   // Balanced work split: this CTA owns strip-rows [q0, q1) of the strip-major
   // (strip, output row) space; it walks them as one segment per strip touched.
   const long long range = P.r_hi - P.r_lo;
   const long long q0 = (long long)blockIdx.x * P.chunk;
   const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * range);
-  // segment geometry at position q (identical in every role); returns the
-  // position after the segment
   auto seg_geom = [&](long long q, int &v0, int &A, int &Bn, int &R0, int &R1) -> long long {
     const int s = (int)(q / range);
     const long long end = min(q1, (long long)(s + 1) * range);
@@ -290,287 +382,299 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_pass_kernel(const __grid_const
     return end;
   };
 
-  if (warp == 0) {
-    // ===================== MMA issuer (one thread) ============================
-    if (lane == 0) {
-      uint32_t ph_afull = 0, ph_free = 0;
-      for (long long q = q0; q < q1;) {
-        int v0, A, Bn, R0, R1;
-        q = seg_geom(q, v0, A, Bn, R0, R1);
-        for (int t = A; t < Bn + 2 * (G - 1); ++t) {
-          rev_for<G>([&](auto JC) {
-            constexpr int j = decltype(JC)::value;
-            const int r = t - 2 * j;
-            if (r >= A && r < Bn) {
-              const int q = r & 1;
-              mbar_wait(a_full(j, q), (ph_afull >> (2 * j + q)) & 1);
-              ph_afull ^= 1u << (2 * j + q);
-              mbar_wait(acc_free(j), (ph_free >> j) & 1);
-              ph_free ^= 1u << j;
+  const int wq = warp & 3;                 // lane quarter == warp index within the group
+  const int l = wq * 32 + lane;            // strip lane (pixel) of this thread
+  const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16);
+
+  auto group = [&](auto JC) {
+    constexpr int j = decltype(JC)::value;
+    constexpr int kind = PL::kind(j), ns = PL::ns(j), nk = PL::nk(j);
+    constexpr bool LINK_IN = kind == K_C2 && !PL::global_resid(j);
+    constexpr bool GRES = PL::global_resid(j) && !HI;
+    uint32_t ph_acc = 0, ph_af = 0, ph_ae = 0, ph_ain = 0, ph_lf = 0, ph_le = 0;
+    float vals[32];
+    // layer 0: pass-input rows / global-residual conv2: residual rows, prefetched
+    // two rows ahead (aux = next row to use, aux2 = the one after)
+    float aux[32], aux2[32];
+    PROF_DECL
+    for (long long qq = q0; qq < q1;) {
+      int v0, A, Bn, R0, R1;
+      qq = seg_geom(qq, v0, A, Bn, R0, R1);
+      const int v = v0 + l;
+      const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
+      const bool in_img = v >= 0 && v < P.VW && col < P.W;
+      const bool lane_valid = l >= G && l < G + P.S && v >= 0 && v < P.VW;
+      // pass buffers are channel-group planar: [row][group of 4 channels][v][4]
+      auto xoff = [&](int row, int g) { return ((size_t)row * 8 + g) * P.VW + v; };
+      auto load_row32 = [&](int row, float (&dst)[32]) {   // fp32 x row (0 outside)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) dst[i] = 0.f;
+        if (row < Bn && v >= 0 && v < P.VW) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(row, g));
+            dst[4 * g] = f.x; dst[4 * g + 1] = f.y; dst[4 * g + 2] = f.z; dst[4 * g + 3] = f.w;
+          }
+        }
+      };
+      auto load_in = [&](int row, float (&dst)[32]) {      // pass input row
+        if constexpr (HI) {
+          dst[0] = dst[1] = 0.f;
+          if (in_img && row < Bn) {
+            const size_t idx = ((size_t)b * P.rows + row) * P.W + col;
+            dst[0] = __ldg(P.c + idx);
+            dst[1] = __ldg(P.z + idx);
+          }
+        } else {
+          load_row32(row, dst);
+        }
+      };
+      // rotate the two-deep prefetch: aux <- aux2, aux2 <- row
+      auto advance = [&](int row) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) aux[i] = aux2[i];
+        if constexpr (j == 0) load_in(row, aux2);
+        else load_row32(row, aux2);
+      };
+      if constexpr (j == 0) { load_in(A, aux); load_in(A + 1, aux2); }
+      if constexpr (GRES) { load_row32(A, aux); load_row32(A + 1, aux2); }
+      // a warp whose 32 pixels are all inside the image skips the zero padding
+      const bool warp_in = __all_sync(0xffffffffu, in_img);
+      const int t_end = Bn + 2 * (G - 1);
+      int tm3 = ((A - 2 - 2 * j) % 3 + 3) % 3;   // (r - 1) mod 3 at t = A - 2, tracked incrementally
+      for (int t = A - 2; t <= t_end; ++t) {
+        const int r = t - 2 * j;
+        const int d = r - 1, e = r + 2;
+        const int slot = tm3;                      // slot of rows d and e (e = d + 3)
+        tm3 = tm3 == 2 ? 0 : tm3 + 1;
+        if (r < A - 2 || r > Bn) continue;         // layer idle at this step
+        auto &resbuf = aux;
+        auto &inbuf = aux;
+        PROF_MARK(0);
+        // ---- 1. wait for MMA(r)
+        if (r >= A && r < Bn) {
+          if (lane == 0) mbar_wait(acc_full(j), ph_acc & 1);
+          ph_acc ^= 1u;
+          __syncwarp();
+          tc_fence_after();
+        }
+        PROF_MARK(1);
+        const uint32_t taddr = tlane + PL::tcol(j) + slot * ns;
+        // ---- 2. finished row d -> registers
+        const bool drain = d >= A && d < Bn;
+        if (drain) {
+          if constexpr (kind == K_OUT) vals[0] = tmem_ld1(taddr);
+          else tmem_ld32(taddr, vals);
+        }
+        PROF_MARK(2);
+        // ---- 3. re-initialise the slot for row e: zero (bias is added at
+        //         hand-off) or, for a conv2, residual + bias
+        if (e >= A && e < Bn) {
+          if constexpr (kind == K_C2) {
+            if constexpr (LINK_IN) {
+              const int lq = e & 1;
+              if (lane == 0) mbar_wait(link_full(lq), (ph_lf >> lq) & 1);
+              ph_lf ^= 1u << lq;
+              __syncwarp();
               tc_fence_after();
-              const int rot = r % 3;
-              const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);
-              constexpr int ns = PL::ns(j), nk = PL::nk(j);
-              constexpr uint32_t idesc = idesc_f16(3 * ns);
-              const uint32_t a_base = sbase + PL::a_off(j) + q * PL::abytes(j);
-              const uint32_t w_base = sbase + PL::w_off(j) + o * ns * 16;
-              const uint32_t d = tmem + PL::tcol(j);
+              tmem_ld32(tlane + PL::LINK_COL + lq * 32, resbuf);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(link_empty(lq));
 #pragma unroll
-              for (int kx = 0; kx < 3; ++kx) {
+              for (int i = 0; i < 32; ++i) resbuf[i] += PBIAS(j, i);
+              tmem_st32(taddr, resbuf);
+            } else {
 #pragma unroll
-                for (int kh = 0; kh < nk; ++kh) {
-                  const uint64_t ad = umma_desc(a_base + kh * 2 * PLANE + kx * 16, PLANE, 128);
-                  const uint64_t bd = umma_desc(w_base + (kx * nk + kh) * tile_bytes(ns),
-                                                NSLICE * ns * 16, 128);
-                  tc_mma(d, ad, bd, idesc);
-                }
-              }
-              tc_commit(a_empty(j, q));
-              tc_commit(acc_full(j));
-              TRACE("MMA t=%d j=%d r=%d issued\n", t, j, r);
+              for (int i = 0; i < 32; ++i) resbuf[i] += PBIAS(j, i);
+              tmem_st32(taddr, resbuf);
+              if constexpr (GRES) advance(e + 2);
             }
-            // no commit on the drain-only step r == Bn: the last row's data is
-            // covered by the previous completion, and two back-to-back
-            // completions could let a slow waiter miss a parity phase
-          });
-        }
-      }
-    }
-  } else {
-    // ===================== epilogue: two warp sets ============================
-    // Set s handles the layers j with j % 2 == s (a conv2 and the layer that
-    // holds its residual are two layers apart, so they share a set and the fp32
-    // residual rows stay in the same thread's registers).  Within a set the 8
-    // warps cover the 4 TMEM lane quarters x 2 channel halves.  Set 0 also
-    // streams the pass input rows into layer 0's A buffer, one row ahead, with
-    // the global loads prefetched a further row ahead in registers.
-    const int ew = (warp - 1) & 7;
-    const int quarter = warp & 3, hf = ew >> 2;
-    const int l = quarter * 32 + lane;
-    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16);
-    // one code path per set: the compiler then only keeps that set's
-    // register arrays live (held / pre for conv2 residuals, pf for loads)
-    auto epilogue = [&](auto SETC) {
-      constexpr int set = decltype(SETC)::value;
-      uint32_t ph_full = 0, ph_empty = 0, ph_in = 0;
-      float held[2][16];
-      float pre[16];
-      constexpr int NV = HI ? 2 : 16;
-      float pf[NV];
-  #pragma unroll
-      for (int i = 0; i < 16; ++i) { held[0][i] = held[1][i] = pre[i] = 0.f; }
-      for (long long qq = q0; qq < q1;) {
-        int v0, A, Bn, R0, R1;
-        qq = seg_geom(qq, v0, A, Bn, R0, R1);
-        const int v = v0 + l;
-        const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
-        const bool in_img = v >= 0 && v < P.VW && col < P.W;
-        const bool lane_valid = l >= G && l < G + P.S && v >= 0 && v < P.VW;
-        // pass buffers are channel-group planar: [row][group of 4 channels][v][4]
-        // (float4 index), so a warp's 16-byte accesses are 512 contiguous bytes
-        auto xoff = [&](int row, int g) { return ((size_t)row * 8 + g) * P.VW + v; };
-        auto load_resid = [&](int e) {
-  #pragma unroll
-          for (int i = 0; i < 16; ++i) pre[i] = 0.f;
-          if constexpr (!HI) {
-            if (e < Bn && v >= 0 && v < P.VW) {
-  #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(e, 4 * hf + i));
-                pre[4 * i] = f.x; pre[4 * i + 1] = f.y; pre[4 * i + 2] = f.z; pre[4 * i + 3] = f.w;
-              }
-            }
-          }
-        };
-        if constexpr (!HI) {
-          if (set == 1) load_resid(A);   // layer 1 (a conv2) takes its residual from the pass input
-        }
-        // pass input row t -> registers (set 0): (c, z) or 16 channels of x
-        auto load_in = [&](int t) {
-  #pragma unroll
-          for (int i = 0; i < NV; ++i) pf[i] = 0.f;
-          if (!in_img || t >= Bn) return;
-          if constexpr (HI) {
-            const size_t idx = ((size_t)b * P.rows + t) * P.W + col;
-            pf[0] = __ldg(P.c + idx);
-            pf[1] = __ldg(P.z + idx);
+          } else if constexpr (kind == K_OUT) {
+            tmem_st16_zero(taddr);
           } else {
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(t, 4 * hf + i));
-              pf[4 * i] = f.x; pf[4 * i + 1] = f.y; pf[4 * i + 2] = f.z; pf[4 * i + 3] = f.w;
+            tmem_st32_zero(taddr);
+          }
+        }
+        PROF_MARK(3);
+        // ---- 4. layer 0: pass-input row r+1 -> A buffer
+        const int rn = r + 1;
+        const bool issue = rn >= A && rn < Bn;
+        if constexpr (j == 0) {
+          if (issue) {
+            const int q = rn & 1;
+            if (rn - 2 >= A) {
+              if (lane == 0) mbar_wait(a_empty(0, q), (ph_ain >> q) & 1);
+              ph_ain ^= 1u << q;
+              __syncwarp();
             }
-          }
-        };
-        // registers (row t) -> layer 0's A buffer, then prefetch row t+1
-        auto store_in = [&](int t) {
-          const int q = t & 1;
-          if (t - 2 >= A) {
-            if (lane == 0) mbar_wait(a_empty(0, q), (ph_in >> q) & 1);
-            ph_in ^= 1u << q;
-            __syncwarp();
-          }
-          const uint32_t dst = sbase + PL::a_off(0) + q * PL::abytes(0) + (l + 1) * 16;
-          if constexpr (HI) {
-            if (hf == 0) {
+            const uint32_t dst = sbase + PL::a_off(0) + q * PL::abytes(0) + (l + 1) * 16;
+            if constexpr (HI) {
               // K=16 channel slots: [c_hi, c_lo, c_hi, z_hi, z_lo, z_hi, 0, 0 | 0 x 8]
-              const __half ch = __float2half_rn(pf[0]);
-              const __half cl = __float2half_rn(pf[0] - __half2float(ch));
-              const __half zh = __float2half_rn(pf[1]);
-              const __half zl = __float2half_rn(pf[1] - __half2float(zh));
+              const __half ch = __float2half_rn(inbuf[0]);
+              const __half cl = __float2half_rn(inbuf[0] - __half2float(ch));
+              const __half zh = __float2half_rn(inbuf[1]);
+              const __half zl = __float2half_rn(inbuf[1] - __half2float(zh));
               __half2 p0 = __halves2half2(ch, cl), p1 = __halves2half2(ch, zh), p2 = __halves2half2(zl, zh);
               st_shared_v4(dst, *reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1),
                            *reinterpret_cast<uint32_t *>(&p2), 0u);
+            } else {
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4)
+                st_shared_v4(dst + c4 * PLANE, pack_h2(inbuf[8 * c4], inbuf[8 * c4 + 1]),
+                             pack_h2(inbuf[8 * c4 + 2], inbuf[8 * c4 + 3]), pack_h2(inbuf[8 * c4 + 4], inbuf[8 * c4 + 5]),
+                             pack_h2(inbuf[8 * c4 + 6], inbuf[8 * c4 + 7]));
+            }
+            fence_proxy_async();
+            advance(rn + 2);
+          }
+        }
+        PROF_MARK(4);
+        // ---- 5. hand off row d
+        if (drain) {
+          if constexpr (kind == K_OUT) {
+            const float logit = vals[0] + PBIAS(j, 0);
+            if (lane_valid && in_img && d >= R0 && d < R1) {
+              if (!isfinite(logit)) atomicOr(P.flag, 1);
+              const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
+              if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
+              if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
             }
           } else {
-            const uint32_t d2 = dst + (2 * hf) * PLANE;
-            st_shared_v4(d2, pack_h2(pf[0], pf[1]), pack_h2(pf[2], pf[3]), pack_h2(pf[4], pf[5]),
-                         pack_h2(pf[6], pf[7]));
-            st_shared_v4(d2 + PLANE, pack_h2(pf[8], pf[9]), pack_h2(pf[10], pf[11]), pack_h2(pf[12], pf[13]),
-                         pack_h2(pf[14], pf[15]));
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(a_full(0, q));
-          if (lane == 0) TRACE("LOAD warp %d stored row %d\n", warp, t);
-          load_in(t + 1);
-        };
-        if (set == 0) load_in(A);
-        for (int t = A - 2; t <= Bn + 2 * (G - 1); ++t) {
-          rev_for<G>([&](auto JC) {
-            constexpr int j = decltype(JC)::value;
-            if constexpr ((j & 1) != set) return;
-            else {
-            constexpr int kind = PL::kind(j), ns = PL::ns(j);
-            const int r = t - 2 * j;
-            if (r >= A && r < Bn) {
-              if (lane == 0) mbar_wait(acc_full(j), (ph_full >> j) & 1);
-              if (lane == 0) TRACE("EPI warp %d t=%d j=%d acc_full ok\n", warp, t, j);
-              ph_full ^= 1u << j;
-              __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float x = vals[i];
+              if constexpr (kind != K_C2) x += PBIAS(j, i);
+              if constexpr (kind == K_C1) x = fmaxf(x, 0.f);
+              vals[i] = x;
+            }
+            if (!warp_in) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) vals[i] = in_img ? vals[i] : 0.f;
+            }
+            if constexpr (PL::holds(j)) {
+              const int lq = d & 1;
+              if (d - 2 >= A) {
+                if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
+                ph_le ^= 1u << lq;
+                __syncwarp();
+              }
               tc_fence_after();
-            }
-            const int d = r - 1, e = r + 2;
-            const bool do_drain = d >= A && d < Bn;
-            const bool do_init = e >= A && e < Bn;
-            // ---- 1. load the finished row d from TMEM ----
-            float val[16];
-            float logit = 0.f;
-            if (do_drain) {
-              const uint32_t taddr = tlane + PL::tcol(j) + (d % 3) * ns;
-              if constexpr (kind == K_OUT) {
-                if (hf == 0) logit = tmem_ld1(taddr);
-              } else {
-                tmem_ld16(taddr + hf * 16, val);
-              }
-            }
-            // ---- 2. initialise slot of row e (same slot as d: after the load) and
-            //         release the MMA for this layer's next row ----
-            if (do_init) {
-              // in place: the held / prefetched residual row is consumed exactly once
-              const uint32_t taddr = tlane + PL::tcol(j) + (e % 3) * ns;
-              if constexpr (kind == K_C2) {
-                if constexpr (j >= 2 && PL::holds(j >= 2 ? j - 2 : 0)) {
-                  constexpr int hi_ = PL::hold_idx(j - 2);
-  #pragma unroll
-                  for (int i = 0; i < 16; ++i) held[hi_][i] += bias_s[j * 32 + hf * 16 + i];
-                  tmem_st16(taddr + hf * 16, held[hi_]);
-                } else {
-  #pragma unroll
-                  for (int i = 0; i < 16; ++i) pre[i] += bias_s[j * 32 + hf * 16 + i];
-                  tmem_st16(taddr + hf * 16, pre);
-                }
-              } else if (kind != K_OUT || hf == 0) {
-                tmem_st16_zero(taddr + (kind == K_OUT ? 0 : hf * 16));
-              }
-            }
-            if (r + 1 >= A && r + 1 < Bn) {
+              tmem_st32(tlane + PL::LINK_COL + lq * 32, vals);
               tmem_wait_st();
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(acc_free(j));
+              if (lane == 0) mbar_arrive(link_full(lq));
             }
-            if constexpr (kind == K_C2 && !(j >= 2 && PL::holds(j >= 2 ? j - 2 : 0))) {
-              if (do_init) load_resid(e + 1);
-            }
-            // ---- 3. epilogue math + hand-off of row d ----
-            if (do_drain) {
-              if constexpr (kind == K_OUT) {
-                if (hf == 0) {
-                  logit += bias_s[j * 32];
-                  if (lane_valid && in_img && d >= R0 && d < R1) {
-                    if (!isfinite(logit)) atomicOr(P.flag, 1);
-                    const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
-                    if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
-                    if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
-                  }
-                }
-              } else {
-  #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  float x = val[i];
-                  if constexpr (kind == K_IN) x += bias_s[j * 32 + hf * 16 + i];
-                  if constexpr (kind == K_C1) x = fmaxf(x + bias_s[j * 32 + hf * 16 + i], 0.f);
-                  val[i] = in_img ? x : 0.f;
-                }
-                if constexpr (PL::holds(j)) {
-  #pragma unroll
-                  for (int i = 0; i < 16; ++i) held[PL::hold_idx(j)][i] = val[i];
-                }
-                if constexpr (PL::feeds_next(j)) {
-                  const int q = d & 1;
-                  if (d - 2 >= A) {
-                    if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
-                    ph_empty ^= 1u << (2 * (j + 1) + q);
-                    __syncwarp();
-                  }
-                  const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16 +
-                                       (2 * hf) * PLANE;
-                  st_shared_v4(dst, pack_h2(val[0], val[1]), pack_h2(val[2], val[3]), pack_h2(val[4], val[5]),
-                               pack_h2(val[6], val[7]));
-                  st_shared_v4(dst + PLANE, pack_h2(val[8], val[9]), pack_h2(val[10], val[11]),
-                               pack_h2(val[12], val[13]), pack_h2(val[14], val[15]));
-                  fence_proxy_async();
-                  __syncwarp();
-                  if (lane == 0) mbar_arrive(a_full(j + 1, q));
-                } else {
-                  // last layer of a non-output pass: fp32 x -> global
-                  if (lane_valid && d >= R0 && d < R1) {
-                    float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
-  #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                      dstg[xoff(d, 4 * hf + i)] = make_float4(val[4 * i], val[4 * i + 1], val[4 * i + 2], val[4 * i + 3]);
-                  }
-                }
+            if constexpr (PL::feeds_next(j)) {
+              const int q = d & 1;
+              PROF_MARK(9);
+              if (d - 2 >= A) {
+                if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
+                ph_ae ^= 1u << q;
+                __syncwarp();
+              }
+              PROF_MARK(10);
+              const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16;
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4)
+                st_shared_v4(dst + c4 * PLANE, pack_h2(vals[8 * c4], vals[8 * c4 + 1]),
+                             pack_h2(vals[8 * c4 + 2], vals[8 * c4 + 3]), pack_h2(vals[8 * c4 + 4], vals[8 * c4 + 5]),
+                             pack_h2(vals[8 * c4 + 6], vals[8 * c4 + 7]));
+              PROF_MARK(11);
+              fence_proxy_async();
+              PROF_MARK(12);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(a_full(j + 1, q));
+              PROF_MARK(13);
+            } else {
+              // last layer of a non-output pass: fp32 x -> global
+              if (lane_valid && d >= R0 && d < R1) {
+                float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                  dstg[xoff(d, g)] = make_float4(vals[4 * g], vals[4 * g + 1], vals[4 * g + 2], vals[4 * g + 3]);
               }
             }
-            }  // layer of this set
-          });
-          if (set == 0 && t + 1 >= A && t + 1 < Bn) store_in(t + 1);
-        }
-        // consume the trailing a_empty completions of the buffers we produce into
-  #pragma unroll
-        for (int j = 0; j + 1 < G; ++j) {
-          if ((j & 1) != set) continue;
-          for (int t = max(A, Bn - 2); t < Bn; ++t) {
-            const int q = t & 1;
-            if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_empty >> (2 * (j + 1) + q)) & 1);
-            ph_empty ^= 1u << (2 * (j + 1) + q);
           }
         }
-        if (set == 0) {
-          for (int t = max(A, Bn - 2); t < Bn; ++t) {
-            const int q = t & 1;
-            if (lane == 0) mbar_wait(a_empty(0, q), (ph_in >> q) & 1);
-            ph_in ^= 1u << q;
+        PROF_MARK(5);
+        // ---- 6. group barrier, then issue MMA(r+1)
+        if (issue) {
+          tmem_wait_st();
+          tc_fence_before();
+          named_bar(1 + j, 128);
+          PROF_MARK(6);
+          if (wq == 0) {
+            const int q = rn & 1;
+            if constexpr (j > 0) {
+              if (lane == 0) mbar_wait(a_full(j, q), (ph_af >> q) & 1);
+              ph_af ^= 1u << q;
+            }
+            __syncwarp();
+            PROF_MARK(7);
+            tc_fence_after();
+            int rot = (slot + 1) % 3;              // (r+1) mod 3 = ((r-1) mod 3 + 2) mod 3
+            rot = (slot + 2) % 3;
+            const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);
+            constexpr uint32_t idesc = idesc_f16(3 * ns);
+            constexpr uint32_t lbo_b = NSLICE * ns * 16;
+            const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
+            const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)(lbo_b >> 4) << 16);
+            const uint32_t a_add = (PL::a_off(j) + q * PL::abytes(j)) >> 4;
+            const uint32_t b_add = (PL::w_off(j) + o * ns * 16) >> 4;
+            const uint32_t dcol = tmem + PL::tcol(j);
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+#pragma unroll
+              for (int kh = 0; kh < nk; ++kh) {
+                const uint64_t ad = adesc0 + a_add + ((kh * 2 * PLANE + kx * 16) >> 4);
+                const uint64_t bd = bdesc0 + b_add + (((kx * nk + kh) * tile_bytes(ns)) >> 4);
+                tc_mma_elect(dcol, ad, bd, idesc);
+              }
+            }
+            if (lane == 0) {
+              tc_commit(a_empty(j, q));
+              tc_commit(acc_full(j));
+            }
+            __syncwarp();
+            PROF_MARK(8);
           }
         }
-        __syncwarp();
       }
-    };
-    if (((warp - 1) >> 3) == 0) epilogue(std::integral_constant<int, 0>{});
-    else epilogue(std::integral_constant<int, 1>{});
-  }
+      // consume the trailing completions this group waits on as a producer
+      if constexpr (PL::feeds_next(j)) {
+        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
+          const int q = rr & 1;
+          if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
+          ph_ae ^= 1u << q;
+        }
+      }
+      if constexpr (j == 0) {
+        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
+          const int q = rr & 1;
+          if (lane == 0) mbar_wait(a_empty(0, q), (ph_ain >> q) & 1);
+          ph_ain ^= 1u << q;
+        }
+      }
+      if constexpr (PL::holds(j)) {
+        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
+          const int lq = rr & 1;
+          if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
+          ph_le ^= 1u << lq;
+        }
+      }
+      __syncwarp();
+    }
+    if (wq < 2 && !HO && !HI) PROF_DUMP(j * 2 + wq);
+  };
+  // dispatch: warps [4j, 4j+4) run layer j
+  const int grp = warp >> 2;
+  if constexpr (G >= 1) { if (grp == 0) group(std::integral_constant<int, 0>{}); }
+  if constexpr (G >= 2) { if (grp == 1) group(std::integral_constant<int, 1>{}); }
+  if constexpr (G >= 3) { if (grp == 2) group(std::integral_constant<int, 2>{}); }
+  if constexpr (G >= 4) { if (grp == 3) group(std::integral_constant<int, 3>{}); }
+
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -664,6 +768,7 @@ struct PassDesc {
 template <bool HI, int NBK, bool HO>
 static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
   using PL = Plan<HI, NBK, HO>;
+  static_assert(PL::G <= 4, "at most 4 layers per pass");
   static_assert(PL::TCOLS <= 512, "TMEM columns exceeded");
   static_assert(PL::SMEM <= 232448, "shared memory exceeded");
   auto kern = tc_pass_kernel<HI, NBK, HO>;
@@ -673,7 +778,7 @@ static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
     attr = true;
   }
   timing_mark_begin(st, (HI ? 100 : 0) + NBK * 10 + (HO ? 1 : 0));
-  kern<<<grid, NTHREADS, PL::SMEM, st>>>(prm);
+  kern<<<grid, 128 * PL::G, PL::SMEM, st>>>(prm);
   timing_mark_end(st);
   count_launch();
   HT_CHECK_LAUNCH();
@@ -697,12 +802,16 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
   PassDesc passes[64];
   int np = 0;
   {
-    const int nb0 = NB < 2 ? NB : 2;
+    // <= 4 layers per pass: conv_in + 1 block | 2 blocks ... | <=1 block + conv_out
+    const int nb0 = NB < 1 ? NB : 1;
     passes[np++] = {true, false, nb0, 0};
     int done = nb0;
-    while (NB - done > 2) { passes[np++] = {false, false, 2, 1 + 2 * done}; done += 2; }
+    while (NB - done > 1) { passes[np++] = {false, false, 2, 1 + 2 * done}; done += 2; }
     passes[np++] = {false, true, NB - done, 1 + 2 * done};
   }
+  HT_REQUIRE(bias_floats(NB) <= MAX_BIAS, "too many layers for the bias bank");
+  HT_CUDA(cudaMemcpyToSymbolAsync(c_bias, tc_b, sizeof(float) * bias_floats(NB), 0,
+                                  cudaMemcpyDeviceToDevice, st));
   const uint8_t *wbase = (const uint8_t *)tc_w;
   const float *in_x = nullptr;
   float *out_x = xa;
@@ -711,7 +820,7 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     const int G = (pd.hi ? 1 : 0) + 2 * pd.nbk + (pd.ho ? 1 : 0);
     TcParams prm{};
     prm.w = wbase + (pd.layer0 == 0 ? 0 : weight_offset_mid(pd.layer0 - 1));
-    prm.bias = tc_b + 32 * pd.layer0;
+    prm.layer0 = pd.layer0;
     prm.c = c; prm.z = z;
     prm.x_in = in_x;
     prm.x_out = pd.ho ? nullptr : out_x;
@@ -732,11 +841,9 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     grid = (total + prm.chunk - 1) / prm.chunk;
     const int g = (int)grid;
     int rc;
-    if (pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<true, 2, false>(prm, g, st);
-    else if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, g, st);
+    if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, g, st);
     else if (pd.hi && pd.nbk == 0 && !pd.ho) rc = launch_pass<true, 0, false>(prm, g, st);
     else if (!pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<false, 2, false>(prm, g, st);
-    else if (!pd.hi && pd.nbk == 2 && pd.ho) rc = launch_pass<false, 2, true>(prm, g, st);
     else if (!pd.hi && pd.nbk == 1 && pd.ho) rc = launch_pass<false, 1, true>(prm, g, st);
     else if (!pd.hi && pd.nbk == 0 && pd.ho) rc = launch_pass<false, 0, true>(prm, g, st);
     else return fail(HT_E_UNSUPPORTED, "no kernel for pass (hi=%d nbk=%d ho=%d)", pd.hi, pd.nbk, pd.ho);
@@ -749,3 +856,19 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
 
 }  // namespace tc
 }  // namespace ht
+
+#ifdef HT_PROF
+extern "C" int ht_debug_prof(long long *host) {
+  cudaMemcpyFromSymbol(host, ht::tc::g_prof, sizeof(long long) * 128);
+  return 0;
+}
+#endif
+#ifdef HT_TIMELINE
+extern "C" int ht_debug_timeline(long long *host) {
+  cudaMemcpyFromSymbol(host, ht::tc::g_tl, sizeof(long long) * 4 * 4 * 16384);
+  cudaMemset(nullptr, 0, 0);
+  static long long zeros[4 * 4 * 16384];
+  cudaMemcpyToSymbol(ht::tc::g_tl, zeros, sizeof(zeros));
+  return 0;
+}
+#endif
