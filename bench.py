@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=64)
+    ap.add_argument("--workload", default="halftone", choices=["halftone", "train"],
+                    help="halftone = BASELINE config 2 (headline); train = config 5 train_step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -179,6 +181,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, rank, world, B, H, W)
+    if args.workload == "train":
+        return run_train(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -271,13 +275,14 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(str(MID_TAG))
+        try:   # measured DRAM bytes/pixel of this kernel (ncu) x pixels per launch
+            traffic = round(json.load(open(tpath))[str(MID_TAG)]["bytes_per_px"] * px_rank)
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sustained,
                 "unit": "TFLOP/s", "frac": round(achieved / sustained, 4), "traffic": traffic,
                 "kernel": "tc_pass_kernel<false,2,false> (2 residual blocks = 4 convs 32->32)",
+                "traffic_unit": "bytes per launch (DRAM read+write, ncu)",
                 "algorithmic_flop_per_launch": FLOP_PER_PX_MIDPASS * px_rank,
                 "mean_launch_ms": round(mid_ms, 4), "launches_timed": len(mid),
                 "peak_kind": f"sustained bf16/fp16 dense ({src})",
@@ -304,6 +309,48 @@ def main():
            "gpu_launches": launches_per_step * args.steps,
            "clocks": clk.summary()}
     print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_train(args, rank, world, local):
+    """BASELINE config 5: one rl.train_step = batch 16 of 256x256 crops + 4
+    flat-gray images, forward, LE estimator (Gaussian HVS), anisotropy loss,
+    backward, Adam; data parallel over the ranks with one all-reduce."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    cfg = rl.TrainConfig(iterations=1000, batch_size=16, crop_size=256, anisotropy_batch_size=4,
+                         hvs_model="gaussian")
+    ds = [synth.contone(384, 384, seed=100 + i).astype(np.float64) for i in range(8)]
+    rng = Rng(cfg.seed)
+    net = PolicyNetwork(cfg.channels, cfg.blocks)
+    adam = Adam(net.params())
+    net.init_params(rng)
+    for t in range(args.warmup):
+        rl.train_step(net, adam, ds, cfg, rng, t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for t in range(args.steps):
+        diag = rl.train_step(net, adam, ds, cfg, rng, args.warmup + t)
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(el) / args.steps * 1e3
+        print(json.dumps({"metric": "train steps/s (config 5: 16x256^2 + 4 gray, LE + anisotropy, Adam)",
+                          "value": round(1e3 / ms, 3), "unit": "steps/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+                          "higher_is_better": True, "scaling": "strong", "dtype": "f32 (training kernels)",
+                          "last_diag": diag}))
     if world > 1:
         dist.destroy_process_group()
 

@@ -152,18 +152,8 @@ class TrainConfig:
                                       "local_expectation estimator (rl.py:106-109)")
 
 
-def shard_range(n, rank, world):
-    """Contiguous shard [lo, hi) of n items for `rank` (uneven shards allowed)."""
-    base, rem = divmod(n, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
-
-
-def _dist_info(group=None):
-    torch = _torch()
-    if torch.distributed.is_available() and torch.distributed.is_initialized():
-        return torch.distributed.get_rank(group), torch.distributed.get_world_size(group)
-    return 0, 1
+from .parallel import allreduce_sum_, shard_range  # noqa: E402
+from .parallel import dist_info as _dist_info  # noqa: E402
 
 
 def draw_batch(dataset, cfg, rng):
@@ -226,9 +216,7 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
             loss, dpg = anisotropy_device(pg, part, scale=cfg.w_a / ba)
             net.backward_device(dpg, grad)
             stats[2] += loss.sum()
-    if world > 1:
-        torch.distributed.all_reduce(grad, group=group)
-        torch.distributed.all_reduce(stats, group=group)
+    allreduce_sum_(grad, stats, group=group)   # the step's one exchange
     st = stats.cpu().numpy()
     mean_reward = float(st[0] / bs)
     bin_gap = float(st[1] / (bs * size * size))
