@@ -409,7 +409,11 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
       auto load_row32 = [&](int row, float (&dst)[32]) {   // fp32 x row (0 outside)
 #pragma unroll
         for (int i = 0; i < 32; ++i) dst[i] = 0.f;
+#ifdef HT_KO_GLOAD
+        if (false) {
+#else
         if (row < Bn && v >= 0 && v < P.VW) {
+#endif
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(row, g));
@@ -576,8 +580,13 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
               }
               PROF_MARK(10);
               const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16;
+#ifndef HT_KO_STS
 #pragma unroll
               for (int c4 = 0; c4 < 4; ++c4)
+#else
+              if (vals[0] == 12345.f)
+              for (int c4 = 0; c4 < 4; ++c4)
+#endif
                 st_shared_v4(dst + c4 * PLANE, pack_h2(vals[8 * c4], vals[8 * c4 + 1]),
                              pack_h2(vals[8 * c4 + 2], vals[8 * c4 + 3]), pack_h2(vals[8 * c4 + 4], vals[8 * c4 + 5]),
                              pack_h2(vals[8 * c4 + 6], vals[8 * c4 + 7]));
@@ -589,7 +598,11 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
               PROF_MARK(13);
             } else {
               // last layer of a non-output pass: fp32 x -> global
+#ifdef HT_KO_GSTORE
+              if (vals[0] == 12345.f) {
+#else
               if (lane_valid && d >= R0 && d < R1) {
+#endif
                 float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
 #pragma unroll
                 for (int g = 0; g < 8; ++g)
