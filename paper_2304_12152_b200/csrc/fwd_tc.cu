@@ -6,9 +6,9 @@
 // * Row streaming.  A CTA owns a 128-pixel-wide strip of the "virtual image"
 //   (the B images laid side by side, one zero column between neighbours) and
 //   a band of rows.  Each UMMA M-tile is one strip row: 128 pixels = 128 TMEM
-//   lanes.  The network runs as passes of <=5 conv layers; inside a pass every
+//   lanes.  The network runs as passes of <=4 conv layers; inside a pass every
 //   layer streams rows top to bottom in a diagonal wavefront (layer j consumes
-//   its input row t-2j at step t), so only two input rows per layer live in
+//   its input row t-3j at step t), so three input rows per layer live in
 //   shared memory and the per-pass halo is G columns/rows (G = layers in pass).
 // * Implicit GEMM per input row r of a layer: for each horizontal tap kx and
 //   K half kh, one tcgen05.mma (kind::f16, M=128, N=3*32, K=16) with
@@ -26,11 +26,11 @@
 //   (and hi/lo weights) so its input is represented to ~fp32 accuracy.
 // * Per-layer zero padding (nn.py:50): out-of-image pixels are forced to 0 in
 //   every epilogue; out-of-image rows issue no MMAs.
-// * Roles (544 threads): warp 0 lane 0 issues all MMAs; warps 1-16 are the
-//   epilogue in two sets (even / odd layers); set 0 also loads the pass input rows (TMEM -> registers -> bias,
-//   ReLU, fp16 -> next layer's shared-memory row / global x / p,h).
-//   Producer/consumer hand-offs use mbarriers; tcgen05.commit signals MMA
-//   completion.
+// * Roles (128*G threads): one 4-warp group per layer drains its TMEM ring,
+//   re-initialises slots, issues its own MMAs (elected lane) and hands rows on
+//   (TMEM -> registers -> bias, ReLU, fp16 -> next layer's shared-memory row /
+//   global x / p,h).  Group 0 also loads the pass input rows.  Hand-offs use
+//   mbarriers; tcgen05.commit signals MMA completion.
 #include <cuda_fp16.h>
 
 #include <type_traits>
@@ -51,6 +51,12 @@ __device__ __forceinline__ void rev_for(F &&f) {
 }
 
 enum : int { K_IN = 0, K_C1 = 1, K_C2 = 2, K_OUT = 3 };
+// Wavefront skew: layer j processes input row t - SKEW*j at step t, so a row
+// handed over at step t is consumed at step t+1 and a layer never waits on a
+// hand-off of the same step.
+constexpr int SKEW = 3;
+constexpr int NABUF = 3;   // input-row buffers per layer
+constexpr int NLINK = 4;   // residual rows in flight between a holder and its conv2
 
 template <bool HI, int NBK, bool HO>
 struct Plan {
@@ -64,16 +70,18 @@ struct Plan {
   static constexpr int abytes(int j) { return nk(j) * 2 * PLANE; }
   static constexpr int w_off(int j) { return j == 0 ? 0 : w_off(j - 1) + wbytes(j - 1); }
   static constexpr int W_TOTAL = w_off(G - 1) + wbytes(G - 1);
-  static constexpr int a_off(int j) { return j == 0 ? W_TOTAL : a_off(j - 1) + 2 * abytes(j - 1); }
-  static constexpr int A_END = a_off(G - 1) + 2 * abytes(G - 1);
-  // barriers: a_full[G][2], a_empty[G][2], acc_full[G], link_full[2], link_empty[2]
+  // three input-row buffers per layer: the row being written (step t), the
+  // row read by the MMA issued at step t, the row of the MMA issued at t-1
+  static constexpr int a_off(int j) { return j == 0 ? W_TOTAL : a_off(j - 1) + NABUF * abytes(j - 1); }
+  static constexpr int A_END = a_off(G - 1) + NABUF * abytes(G - 1);
+  // barriers: a_full[G][3], a_empty[G][3], acc_full[G], link_full[4], link_empty[4]
   static constexpr int BAR_OFF = A_END;
-  static constexpr int NBAR = 5 * G + 4;
+  static constexpr int NBAR = 7 * G + 2 * NLINK;
   static constexpr int TMEMP_OFF = BAR_OFF + NBAR * 8;
   static constexpr int SMEM = TMEMP_OFF + 16;
   static constexpr int tcol(int j) { return j == 0 ? 0 : tcol(j - 1) + 3 * ns(j - 1); }
-  static constexpr int LINK_COL = tcol(G - 1) + 3 * ns(G - 1);   // residual link: 2 rows x 32 fp32
-  static constexpr int TCOLS = LINK_COL + 64;
+  static constexpr int LINK_COL = tcol(G - 1) + 3 * ns(G - 1);   // residual link: 4 rows x 32 fp32
+  static constexpr int TCOLS = LINK_COL + 32 * NLINK;
   static constexpr bool feeds_next(int j) { return j < G - 1; }
   // layer j's output is the residual of layer j+2 (a conv2) -> written to the TMEM link
   static constexpr bool holds(int j) {
@@ -229,6 +237,9 @@ __device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// read of a pass buffer row (measured: the L1-allocating path is faster than
+// ld.global.nc.L1::no_allocate here, 1.75 vs 1.93 ms per mid pass)
+__device__ __forceinline__ float4 ldg_stream(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t *>(&h);
@@ -304,18 +315,20 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // One 4-warp group per layer (128 threads = the 128 pixel lanes of a strip
 // row; warp k of a group owns TMEM lane quarter k; each thread owns one pixel
 // and all 32 channels).  Per step t a group, for its layer j and input row
-// r = t - 2j:
-//   1. waits for MMA(r) to complete (acc_full)
+// r = t - SKEW*j:
+//   1. waits for MMA(r) to complete (acc_full; retires all earlier MMAs too)
 //   2. loads the finished output row d = r-1 from its TMEM slot
-//   3. re-initialises that slot for row e = r+2 (bias, or residual + bias;
+//   3. row d: bias, ReLU, zero padding, residual-link write, fp16 pack
+//   4. re-initialises that slot for row e = r+2 (zero, or residual + bias;
 //      the residual comes from the pass input or from the TMEM link)
-//   4. (layer 0 only) stores pass-input row r+1 into its A buffer
-//   5. hands row d on: activation, link write, fp16 row for the next layer
-//      (or fp32 x to global / p,h for the output layer)
-//   6. group barrier, then one elected thread issues MMA(r+1) (6 UMMAs) once
-//      the previous layer has handed row r+1 over (a_full).
-// A layer's MMA for step t+1 depends on the previous layer's hand-off from
-// step t only, so layers run concurrently and the tensor pipe is shared.
+//   5. (layer 0 only) stores pass-input row r+1 into its A buffer
+//   6. group barrier, then one elected thread issues MMA(r+1) (6 UMMAs); the
+//      previous layer handed row r+1 over at step t-1 (a_full)
+//   7. hands row d on while MMA(r+1) runs: fp16 row into the next layer's A
+//      buffer (d mod 3), or fp32 x to global / p,h for the output layer.
+// With SKEW = 3 no layer waits on a hand-off of the same step, so every group
+// re-issues as soon as its own accumulator is drained and the tensor pipe
+// always has queued work from some layer.
 template <bool HI, int NBK, bool HO>
 __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(const __grid_constant__ TcParams P) {
   using PL = Plan<HI, NBK, HO>;
@@ -326,22 +339,22 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + PL::BAR_OFF;
-  auto a_full = [&](int j, int q) { return bar0 + 8u * (j * 2 + q); };
-  auto a_empty = [&](int j, int q) { return bar0 + 8u * (2 * G + j * 2 + q); };
-  auto acc_full = [&](int j) { return bar0 + 8u * (4 * G + j); };
-  auto link_full = [&](int q) { return bar0 + 8u * (5 * G + q); };
-  auto link_empty = [&](int q) { return bar0 + 8u * (5 * G + 2 + q); };
+  auto a_full = [&](int j, int q) { return bar0 + 8u * (j * NABUF + q); };
+  auto a_empty = [&](int j, int q) { return bar0 + 8u * (NABUF * G + j * NABUF + q); };
+  auto acc_full = [&](int j) { return bar0 + 8u * (2 * NABUF * G + j); };
+  auto link_full = [&](int q) { return bar0 + 8u * (7 * G + q); };
+  auto link_empty = [&](int q) { return bar0 + 8u * (7 * G + NLINK + q); };
 
   // ---- setup: barriers, zeroed row buffers, weights, TMEM --------------------
   if (tid == 0) {
     for (int j = 0; j < G; ++j) {
-      mbar_init(a_full(j, 0), 4);   // the producing group's 4 warps
-      mbar_init(a_full(j, 1), 4);
-      mbar_init(a_empty(j, 0), 1);  // tcgen05.commit
-      mbar_init(a_empty(j, 1), 1);
+      for (int q = 0; q < NABUF; ++q) {
+        mbar_init(a_full(j, q), 4);   // the producing group's 4 warps
+        mbar_init(a_empty(j, q), 1);  // tcgen05.commit
+      }
       mbar_init(acc_full(j), 1);
     }
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NLINK; ++q) {
       mbar_init(link_full(q), 4);
       mbar_init(link_empty(q), 4);
     }
@@ -391,11 +404,11 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
     constexpr int kind = PL::kind(j), ns = PL::ns(j), nk = PL::nk(j);
     constexpr bool LINK_IN = kind == K_C2 && !PL::global_resid(j);
     constexpr bool GRES = PL::global_resid(j) && !HI;
-    uint32_t ph_acc = 0, ph_af = 0, ph_ae = 0, ph_ain = 0, ph_lf = 0, ph_le = 0;
+    uint32_t ph_acc = 0, ph_af = 0, ph_ae = 0, ph_lf = 0, ph_le = 0;
     float vals[32];
     // layer 0: pass-input rows / global-residual conv2: residual rows, prefetched
-    // two rows ahead (aux = next row to use, aux2 = the one after)
-    float aux[32], aux2[32];
+    // one step ahead (aux = next row to use)
+    float aux[32];
     PROF_DECL
     for (long long qq = q0; qq < q1;) {
       int v0, A, Bn, R0, R1;
@@ -416,7 +429,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
 #endif
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
-            const float4 f = __ldg(reinterpret_cast<const float4 *>(P.x_in) + xoff(row, g));
+            const float4 f = ldg_stream(reinterpret_cast<const float4 *>(P.x_in) + xoff(row, g));
             dst[4 * g] = f.x; dst[4 * g + 1] = f.y; dst[4 * g + 2] = f.z; dst[4 * g + 3] = f.w;
           }
         }
@@ -433,29 +446,27 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           load_row32(row, dst);
         }
       };
-      // rotate the two-deep prefetch: aux <- aux2, aux2 <- row
+      // one-row prefetch: aux holds the next row to use; refill after use
       auto advance = [&](int row) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) aux[i] = aux2[i];
-        if constexpr (j == 0) load_in(row, aux2);
-        else load_row32(row, aux2);
+        if constexpr (j == 0) load_in(row, aux);
+        else load_row32(row, aux);
       };
-      if constexpr (j == 0) { load_in(A, aux); load_in(A + 1, aux2); }
-      if constexpr (GRES) { load_row32(A, aux); load_row32(A + 1, aux2); }
+      if constexpr (j == 0) load_in(A, aux);
+      if constexpr (GRES) load_row32(A, aux);
       // a warp whose 32 pixels are all inside the image skips the zero padding
       const bool warp_in = __all_sync(0xffffffffu, in_img);
-      const int t_end = Bn + 2 * (G - 1);
-      int tm3 = ((A - 2 - 2 * j) % 3 + 3) % 3;   // (r - 1) mod 3 at t = A - 2, tracked incrementally
+      const int t_end = Bn + SKEW * (G - 1);
+      int tm3 = ((A - 3 - SKEW * j) % 3 + 3) % 3;   // (r - 1) mod 3 at t = A - 2, tracked incrementally
       for (int t = A - 2; t <= t_end; ++t) {
-        const int r = t - 2 * j;
+        const int r = t - SKEW * j;
         const int d = r - 1, e = r + 2;
-        const int slot = tm3;                      // slot of rows d and e (e = d + 3)
+        const int slot = tm3;                      // slot (and A buffer) of rows d and e (e = d + 3)
         tm3 = tm3 == 2 ? 0 : tm3 + 1;
         if (r < A - 2 || r > Bn) continue;         // layer idle at this step
         auto &resbuf = aux;
         auto &inbuf = aux;
         PROF_MARK(0);
-        // ---- 1. wait for MMA(r)
+        // ---- 1. wait for MMA(r) (it also retires every earlier MMA of this layer)
         if (r >= A && r < Bn) {
           if (lane == 0) mbar_wait(acc_full(j), ph_acc & 1);
           ph_acc ^= 1u;
@@ -471,12 +482,48 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           else tmem_ld32(taddr, vals);
         }
         PROF_MARK(2);
-        // ---- 3. re-initialise the slot for row e: zero (bias is added at
+        // ---- 3. row d: activation, residual link, fp16 pack (early, so only
+        //         16 packed registers stay live across the rest of the step)
+        uint32_t hv[16];
+        if constexpr (kind != K_OUT) {
+          if (drain) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float x = vals[i];
+              if constexpr (kind != K_C2) x += PBIAS(j, i);
+              if constexpr (kind == K_C1) x = fmaxf(x, 0.f);
+              vals[i] = x;
+            }
+            if (!warp_in) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) vals[i] = in_img ? vals[i] : 0.f;
+            }
+            if constexpr (PL::holds(j)) {
+              const int lq = d & (NLINK - 1);
+              if (d - NLINK >= A) {
+                if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
+                ph_le ^= 1u << lq;
+                __syncwarp();
+              }
+              tc_fence_after();
+              tmem_st32(tlane + PL::LINK_COL + lq * 32, vals);
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(link_full(lq));
+            }
+            if constexpr (PL::feeds_next(j)) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) hv[i] = pack_h2(vals[2 * i], vals[2 * i + 1]);
+            }
+          }
+        }
+        // ---- 4. re-initialise the slot for row e: zero (bias is added at
         //         hand-off) or, for a conv2, residual + bias
         if (e >= A && e < Bn) {
           if constexpr (kind == K_C2) {
             if constexpr (LINK_IN) {
-              const int lq = e & 1;
+              const int lq = e & (NLINK - 1);
               if (lane == 0) mbar_wait(link_full(lq), (ph_lf >> lq) & 1);
               ph_lf ^= 1u << lq;
               __syncwarp();
@@ -492,7 +539,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
 #pragma unroll
               for (int i = 0; i < 32; ++i) resbuf[i] += PBIAS(j, i);
               tmem_st32(taddr, resbuf);
-              if constexpr (GRES) advance(e + 2);
+              if constexpr (GRES) advance(e + 1);
             }
           } else if constexpr (kind == K_OUT) {
             tmem_st16_zero(taddr);
@@ -501,18 +548,14 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           }
         }
         PROF_MARK(3);
-        // ---- 4. layer 0: pass-input row r+1 -> A buffer
+        // ---- 5. layer 0: pass-input row r+1 -> A buffer (r+1) mod 3.  Its
+        //         previous row r-2 was read by MMA(r-2), retired by step 1.
         const int rn = r + 1;
+        const int qn = slot == 0 ? 2 : slot - 1;  // (r+1) mod 3
         const bool issue = rn >= A && rn < Bn;
         if constexpr (j == 0) {
           if (issue) {
-            const int q = rn & 1;
-            if (rn - 2 >= A) {
-              if (lane == 0) mbar_wait(a_empty(0, q), (ph_ain >> q) & 1);
-              ph_ain ^= 1u << q;
-              __syncwarp();
-            }
-            const uint32_t dst = sbase + PL::a_off(0) + q * PL::abytes(0) + (l + 1) * 16;
+            const uint32_t dst = sbase + PL::a_off(0) + qn * PL::abytes(0) + (l + 1) * 16;
             if constexpr (HI) {
               // K=16 channel slots: [c_hi, c_lo, c_hi, z_hi, z_lo, z_hi, 0, 0 | 0 x 8]
               const __half ch = __float2half_rn(inbuf[0]);
@@ -530,111 +573,31 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
                              pack_h2(inbuf[8 * c4 + 6], inbuf[8 * c4 + 7]));
             }
             fence_proxy_async();
-            advance(rn + 2);
+            advance(rn + 1);
           }
         }
         PROF_MARK(4);
-        // ---- 5. hand off row d
-        if (drain) {
-          if constexpr (kind == K_OUT) {
-            const float logit = vals[0] + PBIAS(j, 0);
-            if (lane_valid && in_img && d >= R0 && d < R1) {
-              if (!isfinite(logit)) atomicOr(P.flag, 1);
-              const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
-              if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
-              if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float x = vals[i];
-              if constexpr (kind != K_C2) x += PBIAS(j, i);
-              if constexpr (kind == K_C1) x = fmaxf(x, 0.f);
-              vals[i] = x;
-            }
-            if (!warp_in) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) vals[i] = in_img ? vals[i] : 0.f;
-            }
-            if constexpr (PL::holds(j)) {
-              const int lq = d & 1;
-              if (d - 2 >= A) {
-                if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
-                ph_le ^= 1u << lq;
-                __syncwarp();
-              }
-              tc_fence_after();
-              tmem_st32(tlane + PL::LINK_COL + lq * 32, vals);
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(link_full(lq));
-            }
-            if constexpr (PL::feeds_next(j)) {
-              const int q = d & 1;
-              PROF_MARK(9);
-              if (d - 2 >= A) {
-                if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
-                ph_ae ^= 1u << q;
-                __syncwarp();
-              }
-              PROF_MARK(10);
-              const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16;
-#ifndef HT_KO_STS
-#pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4)
-#else
-              if (vals[0] == 12345.f)
-              for (int c4 = 0; c4 < 4; ++c4)
-#endif
-                st_shared_v4(dst + c4 * PLANE, pack_h2(vals[8 * c4], vals[8 * c4 + 1]),
-                             pack_h2(vals[8 * c4 + 2], vals[8 * c4 + 3]), pack_h2(vals[8 * c4 + 4], vals[8 * c4 + 5]),
-                             pack_h2(vals[8 * c4 + 6], vals[8 * c4 + 7]));
-              PROF_MARK(11);
-              fence_proxy_async();
-              PROF_MARK(12);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(a_full(j + 1, q));
-              PROF_MARK(13);
-            } else {
-              // last layer of a non-output pass: fp32 x -> global
-#ifdef HT_KO_GSTORE
-              if (vals[0] == 12345.f) {
-#else
-              if (lane_valid && d >= R0 && d < R1) {
-#endif
-                float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
-#pragma unroll
-                for (int g = 0; g < 8; ++g)
-                  dstg[xoff(d, g)] = make_float4(vals[4 * g], vals[4 * g + 1], vals[4 * g + 2], vals[4 * g + 3]);
-              }
-            }
-          }
-        }
-        PROF_MARK(5);
-        // ---- 6. group barrier, then issue MMA(r+1)
+        // ---- 6. group barrier, then issue MMA(r+1): its input row was handed
+        //         over by layer j-1 at step t-1
         if (issue) {
           tmem_wait_st();
           tc_fence_before();
           named_bar(1 + j, 128);
           PROF_MARK(6);
           if (wq == 0) {
-            const int q = rn & 1;
             if constexpr (j > 0) {
-              if (lane == 0) mbar_wait(a_full(j, q), (ph_af >> q) & 1);
-              ph_af ^= 1u << q;
+              if (lane == 0) mbar_wait(a_full(j, qn), (ph_af >> qn) & 1);
+              ph_af ^= 1u << qn;
             }
             __syncwarp();
             PROF_MARK(7);
             tc_fence_after();
-            int rot = (slot + 1) % 3;              // (r+1) mod 3 = ((r-1) mod 3 + 2) mod 3
-            rot = (slot + 2) % 3;
-            const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);
+            const int o = qn == 0 ? 1 : (qn == 1 ? 0 : 2);   // B window for output rows (r+2, r+1, r)
             constexpr uint32_t idesc = idesc_f16(3 * ns);
             constexpr uint32_t lbo_b = NSLICE * ns * 16;
             const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
             const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)(lbo_b >> 4) << 16);
-            const uint32_t a_add = (PL::a_off(j) + q * PL::abytes(j)) >> 4;
+            const uint32_t a_add = (PL::a_off(j) + qn * PL::abytes(j)) >> 4;
             const uint32_t b_add = (PL::w_off(j) + o * ns * 16) >> 4;
             const uint32_t dcol = tmem + PL::tcol(j);
 #pragma unroll
@@ -647,32 +610,74 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
               }
             }
             if (lane == 0) {
-              tc_commit(a_empty(j, q));
+              if constexpr (j > 0) tc_commit(a_empty(j, qn));
               tc_commit(acc_full(j));
             }
             __syncwarp();
             PROF_MARK(8);
           }
         }
+        // ---- 7. hand row d on (overlaps MMA(r+1))
+        if (drain) {
+          if constexpr (kind == K_OUT) {
+            const float logit = vals[0] + PBIAS(j, 0);
+            if (lane_valid && in_img && d >= R0 && d < R1) {
+              if (!isfinite(logit)) atomicOr(P.flag, 1);
+              const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
+              if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
+              if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
+            }
+          } else if constexpr (PL::feeds_next(j)) {
+            const int q = slot;                  // d mod 3
+            PROF_MARK(9);
+            if (d - NABUF >= A) {
+              if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
+              ph_ae ^= 1u << q;
+              __syncwarp();
+            }
+            PROF_MARK(10);
+            const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16;
+#ifndef HT_KO_STS
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4)
+#else
+            if (hv[0] == 12345u)
+            for (int c4 = 0; c4 < 4; ++c4)
+#endif
+              st_shared_v4(dst + c4 * PLANE, hv[4 * c4], hv[4 * c4 + 1], hv[4 * c4 + 2], hv[4 * c4 + 3]);
+            PROF_MARK(11);
+            fence_proxy_async();
+            PROF_MARK(12);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full(j + 1, q));
+            PROF_MARK(13);
+          } else {
+            // last layer of a non-output pass: fp32 x -> global
+#ifdef HT_KO_GSTORE
+            if (vals[0] == 12345.f) {
+#else
+            if (lane_valid && d >= R0 && d < R1) {
+#endif
+              float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
+#pragma unroll
+              for (int g = 0; g < 8; ++g)
+                dstg[xoff(d, g)] = make_float4(vals[4 * g], vals[4 * g + 1], vals[4 * g + 2], vals[4 * g + 3]);
+            }
+          }
+        }
+        PROF_MARK(5);
       }
       // consume the trailing completions this group waits on as a producer
       if constexpr (PL::feeds_next(j)) {
-        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
-          const int q = rr & 1;
+        for (int rr = max(A, Bn - NABUF); rr < Bn; ++rr) {
+          const int q = rr % 3;
           if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
           ph_ae ^= 1u << q;
         }
       }
-      if constexpr (j == 0) {
-        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
-          const int q = rr & 1;
-          if (lane == 0) mbar_wait(a_empty(0, q), (ph_ain >> q) & 1);
-          ph_ain ^= 1u << q;
-        }
-      }
       if constexpr (PL::holds(j)) {
-        for (int rr = max(A, Bn - 2); rr < Bn; ++rr) {
-          const int lq = rr & 1;
+        for (int rr = max(A, Bn - NLINK); rr < Bn; ++rr) {
+          const int lq = rr & (NLINK - 1);
           if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
           ph_le ^= 1u << lq;
         }
