@@ -14,10 +14,14 @@ buf = (C.c_longlong * 128)()
 # profile the mid pass: run a net whose LAST pass is a mid pass is not possible,
 # so run NB=16 and read (the last writer is the output pass); then NB such that..
 lib.ht_debug_prof(buf)
-names = ["other", "acc_full wait", "tmem ld", "init(+link)", "loader", "hand-off-misc", "group bar", "a_full wait", "mma issue", "act+link", "a_empty wait", "sts", "fence.proxy", "arrive"]
+# v4 step order: 0 loop top, 1 acc_full wait, 2 tmem ld, 3 act+link+pack+init,
+# 4 layer-0 loader, 6 st-wait+named bar, 7 a_full wait, 8 mma issue, 9 pre-hand-off,
+# 10 a_empty wait, 11 sts, 12 fence.proxy, 13 arrive, 5 tail (global store)
+names = ["loop", "acc_full wait", "tmem ld", "act/link/init", "loader", "tail/gstore", "group bar", "a_full wait", "mma issue", "pre-handoff", "a_empty wait", "sts", "fence.proxy", "arrive", "act", "link_empty wait"]
 for g in range(4):
     for w in range(2):
         v = list(buf)[16 * (2 * g + w):16 * (2 * g + w) + 16]
         tot = sum(v)
         if not tot: continue
+        steps = int(sys.argv[2]) if len(sys.argv) > 2 else 0
         print("group", g, "warp", w, "total", tot, " ".join(f"{n}={100*x/tot:.1f}%" for n, x in zip(names, v) if x))

@@ -55,7 +55,12 @@ enum : int { K_IN = 0, K_C1 = 1, K_C2 = 2, K_OUT = 3 };
 // handed over at step t is consumed at step t+1 and a layer never waits on a
 // hand-off of the same step.
 constexpr int SKEW = 3;
-constexpr int NABUF = 3;   // input-row buffers per layer
+// Input-row buffers per layer (Plan::NAB): three decouple producer and
+// consumer fully; two suffice when shared memory is tight (a producer then
+// waits, via a_empty, only for the consumer's MMA issued two steps earlier).
+// A plan takes three when the layout still fits the 196 KB carveout, so the
+// L1 left for the pass-buffer loads stays >= 60 KB.
+constexpr int SMEM_L1_FRIENDLY = 196 * 1024 - 1024;
 constexpr int NLINK = 4;   // residual rows in flight between a holder and its conv2
 
 template <bool HI, int NBK, bool HO>
@@ -70,13 +75,19 @@ struct Plan {
   static constexpr int abytes(int j) { return nk(j) * 2 * PLANE; }
   static constexpr int w_off(int j) { return j == 0 ? 0 : w_off(j - 1) + wbytes(j - 1); }
   static constexpr int W_TOTAL = w_off(G - 1) + wbytes(G - 1);
-  // three input-row buffers per layer: the row being written (step t), the
-  // row read by the MMA issued at step t, the row of the MMA issued at t-1
-  static constexpr int a_off(int j) { return j == 0 ? W_TOTAL : a_off(j - 1) + NABUF * abytes(j - 1); }
-  static constexpr int A_END = a_off(G - 1) + NABUF * abytes(G - 1);
+  // NAB input-row buffers per layer (ring indexed by row)
+  static constexpr int a_bytes_total(int nab) {
+    int t = 0;
+    for (int j = 0; j < G; ++j) t += nab * abytes(j);
+    return t;
+  }
+  static constexpr int NAB =
+      W_TOTAL + A_PHASE + a_bytes_total(3) + ((2 * 3 + 1) * G + 2 * NLINK) * 8 + 16 <= SMEM_L1_FRIENDLY ? 3 : 2;
+  static constexpr int a_off(int j) { return j == 0 ? W_TOTAL + A_PHASE : a_off(j - 1) + NAB * abytes(j - 1); }
+  static constexpr int A_END = a_off(G - 1) + NAB * abytes(G - 1);
   // barriers: a_full[G][3], a_empty[G][3], acc_full[G], link_full[4], link_empty[4]
   static constexpr int BAR_OFF = A_END;
-  static constexpr int NBAR = 7 * G + 2 * NLINK;
+  static constexpr int NBAR = (2 * NAB + 1) * G + 2 * NLINK;
   static constexpr int TMEMP_OFF = BAR_OFF + NBAR * 8;
   static constexpr int SMEM = TMEMP_OFF + 16;
   static constexpr int tcol(int j) { return j == 0 ? 0 : tcol(j - 1) + 3 * ns(j - 1); }
@@ -150,7 +161,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
+#ifdef HT_SPIN
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"
+#endif
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n"
       "DONE_%=:\n\t}" ::"r"(bar),
@@ -190,6 +205,59 @@ __device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint64_t adesc, ui
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1));
 }
+// One row's MMA batch: for kx in 0..2, kh in 0..NK-1 one M=128 x N=3*NS x K=16
+// UMMA with A = a + kh*AK + kx and B = b + (kx*NK + kh)*TB (descriptor units of
+// 16 B), then commit to acc_full (and a_empty when bar_e != 0).  One elect for
+// the whole batch and immediate offsets keep the issue to a few instructions.
+template <int NK, int NS>
+__device__ __forceinline__ void mma_row(uint32_t d, uint64_t a, uint64_t b, uint32_t bar_acc, uint32_t bar_e) {
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)((3 * NS) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  constexpr long long AK = (2 * 2176) >> 4;   // checked against PLANE below
+  constexpr long long TB = (2 * 5 * NS * 16) >> 4;
+  if constexpr (NK == 2) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a1, a2, a3, a4, a5, b1, b2, b3, b4, b5;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "add.s64 a1, %1, %6;\n\tadd.s64 b1, %2, %7;\n\t"
+        "add.s64 a2, %1, 1;\n\tadd.s64 b2, %2, %8;\n\t"
+        "add.s64 a3, %1, %9;\n\tadd.s64 b3, %2, %10;\n\t"
+        "add.s64 a4, %1, 2;\n\tadd.s64 b4, %2, %11;\n\t"
+        "add.s64 a5, %1, %12;\n\tadd.s64 b5, %2, %13;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %14, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %14, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %14, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %14, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %14, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %14, p;\n\t"
+        "and.pred q, q, e;\n\t"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(1), "r"(bar_acc), "r"(bar_e),
+        "n"(AK), "n"(TB), "n"(2 * TB), "n"(AK + 1), "n"(3 * TB), "n"(4 * TB), "n"(AK + 2), "n"(5 * TB),
+        "r"(idesc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a1, a2, b1, b2;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "add.s64 a1, %1, 1;\n\tadd.s64 b1, %2, %6;\n\t"
+        "add.s64 a2, %1, 2;\n\tadd.s64 b2, %2, %7;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %8, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %8, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %8, p;\n\t"
+        "and.pred q, q, e;\n\t"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(1), "r"(bar_acc), "r"(bar_e), "n"(TB), "n"(2 * TB), "r"(idesc)
+        : "memory");
+  }
+}
+static_assert(PLANE == 2176, "mma_row's A chunk offset assumes PLANE == 2176");
+
 // UMMA shared-memory descriptor: K-major, no swizzle, version 1 (sm_100)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
@@ -260,6 +328,7 @@ struct TcParams {
   uint8_t *h;           // HO: (B, out_rows, W) (nullable)
   int *flag;            // HO: non-finite logit flag
   int B, W, VW, rows;   // rows = window rows held by the pass buffers
+  long long pitch;      // pass-buffer pixels per (row, channel group): x_pitch(VW)
   int S, n_strips;      // strip stride (valid lanes) and count
   int r_lo, r_hi;       // output rows [r_lo, r_hi) of this pass (window-relative)
   long long chunk;      // strip-rows per CTA: CTA i owns [i*chunk, (i+1)*chunk) of
@@ -334,6 +403,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   using PL = Plan<HI, NBK, HO>;
   constexpr int G = PL::G;
   constexpr int NT = 128 * G;
+  constexpr int NABUF = PL::NAB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform
@@ -342,8 +412,8 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   auto a_full = [&](int j, int q) { return bar0 + 8u * (j * NABUF + q); };
   auto a_empty = [&](int j, int q) { return bar0 + 8u * (NABUF * G + j * NABUF + q); };
   auto acc_full = [&](int j) { return bar0 + 8u * (2 * NABUF * G + j); };
-  auto link_full = [&](int q) { return bar0 + 8u * (7 * G + q); };
-  auto link_empty = [&](int q) { return bar0 + 8u * (7 * G + NLINK + q); };
+  auto link_full = [&](int q) { return bar0 + 8u * ((2 * NABUF + 1) * G + q); };
+  auto link_empty = [&](int q) { return bar0 + 8u * ((2 * NABUF + 1) * G + NLINK + q); };
 
   // ---- setup: barriers, zeroed row buffers, weights, TMEM --------------------
   if (tid == 0) {
@@ -387,7 +457,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   auto seg_geom = [&](long long q, int &v0, int &A, int &Bn, int &R0, int &R1) -> long long {
     const int s = (int)(q / range);
     const long long end = min(q1, (long long)(s + 1) * range);
-    v0 = s * P.S - G;
+    v0 = s * P.S - STRIP_L;
     R0 = P.r_lo + (int)(q - (long long)s * range);
     R1 = P.r_lo + (int)(end - (long long)s * range);
     A = max(R0 - G, 0);
@@ -405,6 +475,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
     constexpr bool LINK_IN = kind == K_C2 && !PL::global_resid(j);
     constexpr bool GRES = PL::global_resid(j) && !HI;
     uint32_t ph_acc = 0, ph_af = 0, ph_ae = 0, ph_lf = 0, ph_le = 0;
+    TL_DECL
+    // timeline of the mid pass only (CTA 0, warp 0 of each group, lane 0)
+#define TLG(ev) do { if constexpr (!HI && !HO) { if (wq == 0 && lane == 0) TL(j, ev, t, r); } } while (0)
     float vals[32];
     // layer 0: pass-input rows / global-residual conv2: residual rows, prefetched
     // one step ahead (aux = next row to use)
@@ -416,9 +489,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
       const int v = v0 + l;
       const int b = v >= 0 ? v / (P.W + 1) : -1, col = v >= 0 ? v % (P.W + 1) : -1;
       const bool in_img = v >= 0 && v < P.VW && col < P.W;
-      const bool lane_valid = l >= G && l < G + P.S && v >= 0 && v < P.VW;
+      const bool lane_valid = l >= STRIP_L && l < STRIP_L + P.S && v >= 0 && v < P.VW;
       // pass buffers are channel-group planar: [row][group of 4 channels][v][4]
-      auto xoff = [&](int row, int g) { return ((size_t)row * 8 + g) * P.VW + v; };
+      auto xoff = [&](int row, int g) { return ((size_t)row * 8 + g) * P.pitch + v + XPAD; };
       auto load_row32 = [&](int row, float (&dst)[32]) {   // fp32 x row (0 outside)
 #pragma unroll
         for (int i = 0; i < 32; ++i) dst[i] = 0.f;
@@ -474,6 +547,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           tc_fence_after();
         }
         PROF_MARK(1);
+        TLG(1);
         const uint32_t taddr = tlane + PL::tcol(j) + slot * ns;
         // ---- 2. finished row d -> registers
         const bool drain = d >= A && d < Bn;
@@ -482,43 +556,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           else tmem_ld32(taddr, vals);
         }
         PROF_MARK(2);
-        // ---- 3. row d: activation, residual link, fp16 pack (early, so only
-        //         16 packed registers stay live across the rest of the step)
-        uint32_t hv[16];
-        if constexpr (kind != K_OUT) {
-          if (drain) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float x = vals[i];
-              if constexpr (kind != K_C2) x += PBIAS(j, i);
-              if constexpr (kind == K_C1) x = fmaxf(x, 0.f);
-              vals[i] = x;
-            }
-            if (!warp_in) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) vals[i] = in_img ? vals[i] : 0.f;
-            }
-            if constexpr (PL::holds(j)) {
-              const int lq = d & (NLINK - 1);
-              if (d - NLINK >= A) {
-                if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
-                ph_le ^= 1u << lq;
-                __syncwarp();
-              }
-              tc_fence_after();
-              tmem_st32(tlane + PL::LINK_COL + lq * 32, vals);
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(link_full(lq));
-            }
-            if constexpr (PL::feeds_next(j)) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) hv[i] = pack_h2(vals[2 * i], vals[2 * i + 1]);
-            }
-          }
-        }
-        // ---- 4. re-initialise the slot for row e: zero (bias is added at
+        TLG(6);
+        TLG(7);
+        // ---- 3. re-initialise the slot for row e: zero (bias is added at
         //         hand-off) or, for a conv2, residual + bias
         if (e >= A && e < Bn) {
           if constexpr (kind == K_C2) {
@@ -539,7 +579,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
 #pragma unroll
               for (int i = 0; i < 32; ++i) resbuf[i] += PBIAS(j, i);
               tmem_st32(taddr, resbuf);
+#ifndef HT_KO_GRES
               if constexpr (GRES) advance(e + 1);
+#endif
             }
           } else if constexpr (kind == K_OUT) {
             tmem_st16_zero(taddr);
@@ -548,10 +590,12 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           }
         }
         PROF_MARK(3);
-        // ---- 5. layer 0: pass-input row r+1 -> A buffer (r+1) mod 3.  Its
-        //         previous row r-2 was read by MMA(r-2), retired by step 1.
+        TLG(8);
+        // ---- 4. layer 0: pass-input row r+1 -> its A buffer.  The previous
+        //         row there (r+1-NABUF) was read by an MMA retired in step 1.
         const int rn = r + 1;
-        const int qn = slot == 0 ? 2 : slot - 1;  // (r+1) mod 3
+        const int rot = slot == 0 ? 2 : slot - 1;  // (r+1) mod 3: TMEM ring position of row r+1
+        const int qn = NABUF == 3 ? rot : (rn & 1);  // A buffer of row r+1
         const bool issue = rn >= A && rn < Bn;
         if constexpr (j == 0) {
           if (issue) {
@@ -577,13 +621,14 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           }
         }
         PROF_MARK(4);
-        // ---- 6. group barrier, then issue MMA(r+1): its input row was handed
+        // ---- 5. group barrier, then issue MMA(r+1): its input row was handed
         //         over by layer j-1 at step t-1
         if (issue) {
           tmem_wait_st();
           tc_fence_before();
           named_bar(1 + j, 128);
           PROF_MARK(6);
+          TLG(2);
           if (wq == 0) {
             if constexpr (j > 0) {
               if (lane == 0) mbar_wait(a_full(j, qn), (ph_af >> qn) & 1);
@@ -591,30 +636,57 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
             }
             __syncwarp();
             PROF_MARK(7);
+            TLG(3);
             tc_fence_after();
-            const int o = qn == 0 ? 1 : (qn == 1 ? 0 : 2);   // B window for output rows (r+2, r+1, r)
-            constexpr uint32_t idesc = idesc_f16(3 * ns);
+            const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);   // B window for output rows (r+2, r+1, r)
             constexpr uint32_t lbo_b = NSLICE * ns * 16;
             const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
             const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)(lbo_b >> 4) << 16);
             const uint32_t a_add = (PL::a_off(j) + qn * PL::abytes(j)) >> 4;
             const uint32_t b_add = (PL::w_off(j) + o * ns * 16) >> 4;
-            const uint32_t dcol = tmem + PL::tcol(j);
-#pragma unroll
-            for (int kx = 0; kx < 3; ++kx) {
-#pragma unroll
-              for (int kh = 0; kh < nk; ++kh) {
-                const uint64_t ad = adesc0 + a_add + ((kh * 2 * PLANE + kx * 16) >> 4);
-                const uint64_t bd = bdesc0 + b_add + (((kx * nk + kh) * tile_bytes(ns)) >> 4);
-                tc_mma_elect(dcol, ad, bd, idesc);
-              }
-            }
-            if (lane == 0) {
-              if constexpr (j > 0) tc_commit(a_empty(j, qn));
-              tc_commit(acc_full(j));
-            }
+            mma_row<nk, ns>(tmem + PL::tcol(j), adesc0 + a_add, bdesc0 + b_add, acc_full(j),
+                            j > 0 ? a_empty(j, qn) : 0u);
             __syncwarp();
             PROF_MARK(8);
+            TLG(4);
+          }
+        }
+        // ---- 6. row d: activation, residual link, fp16 pack (after the issue:
+        //         off the drain -> issue critical path)
+        uint32_t hv[16];
+        if constexpr (kind != K_OUT) {
+          if (drain) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float x = vals[i];
+              if constexpr (kind != K_C2) x += PBIAS(j, i);
+              if constexpr (kind == K_C1) x = fmaxf(x, 0.f);
+              vals[i] = x;
+            }
+            if (!warp_in) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) vals[i] = in_img ? vals[i] : 0.f;
+            }
+            if constexpr (PL::holds(j)) {
+              const int lq = d & (NLINK - 1);
+              PROF_MARK(14);
+              if (d - NLINK >= A) {
+                if (lane == 0) mbar_wait(link_empty(lq), (ph_le >> lq) & 1);
+                ph_le ^= 1u << lq;
+                __syncwarp();
+              }
+              PROF_MARK(15);
+              tc_fence_after();
+              tmem_st32(tlane + PL::LINK_COL + lq * 32, vals);
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(link_full(lq));
+            }
+            if constexpr (PL::feeds_next(j)) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) hv[i] = pack_h2(vals[2 * i], vals[2 * i + 1]);
+            }
           }
         }
         // ---- 7. hand row d on (overlaps MMA(r+1))
@@ -628,7 +700,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
               if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
             }
           } else if constexpr (PL::feeds_next(j)) {
-            const int q = slot;                  // d mod 3
+            const int q = NABUF == 3 ? slot : (d & 1);   // A buffer of row d
             PROF_MARK(9);
             if (d - NABUF >= A) {
               if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
@@ -666,11 +738,12 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
           }
         }
         PROF_MARK(5);
+        TLG(5);
       }
       // consume the trailing completions this group waits on as a producer
       if constexpr (PL::feeds_next(j)) {
         for (int rr = max(A, Bn - NABUF); rr < Bn; ++rr) {
-          const int q = rr % 3;
+          const int q = rr % NABUF;
           if (lane == 0) mbar_wait(a_empty(j + 1, q), (ph_ae >> q) & 1);
           ph_ae ^= 1u << q;
         }
@@ -774,7 +847,7 @@ int pack(const double *params, int NB, void *tc_dst, float *bias_dst, cudaStream
 int64_t workspace_bytes(int NB, int B, int H, int W, int in_rows) {
   (void)NB; (void)H;
   const int64_t VW = (int64_t)B * (W + 1);
-  return 2 * (int64_t)in_rows * VW * 32 * 4 + 256;
+  return 2 * (int64_t)in_rows * x_pitch((int)VW) * 32 * 4 + 256;
 }
 
 struct PassDesc {
@@ -786,7 +859,7 @@ struct PassDesc {
 template <bool HI, int NBK, bool HO>
 static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
   using PL = Plan<HI, NBK, HO>;
-  static_assert(PL::G <= 4, "at most 4 layers per pass");
+  static_assert(PL::G <= 4 && PL::G <= STRIP_L, "at most 4 layers per pass (halo <= STRIP_L lanes)");
   static_assert(PL::TCOLS <= 512, "TMEM columns exceeded");
   static_assert(PL::SMEM <= 232448, "shared memory exceeded");
   auto kern = tc_pass_kernel<HI, NBK, HO>;
@@ -815,7 +888,7 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
   const int VW = B * (W + 1);
   HT_REQUIRE((int64_t)in_rows * VW * 32 < (1ll << 31) * 16, "image too large");
   float *xa = (float *)ws;
-  float *xb = xa + (size_t)in_rows * VW * 32;
+  float *xb = xa + (size_t)in_rows * x_pitch(VW) * 32;
   // pass plan (layers: conv_in, 2*NB convs, conv_out)
   PassDesc passes[64];
   int np = 0;
@@ -844,7 +917,8 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     prm.x_out = pd.ho ? nullptr : out_x;
     prm.p = p; prm.h = h; prm.flag = flag_dev;
     prm.B = B; prm.W = W; prm.VW = VW; prm.rows = in_rows;
-    prm.S = M - 2 * G;
+    prm.S = STRIP_S;
+    prm.pitch = x_pitch(VW);
     prm.n_strips = (VW + prm.S - 1) / prm.S;
     prm.r_lo = pd.ho ? out_row0 - in_row0 : 0;
     prm.r_hi = pd.ho ? out_row0 - in_row0 + out_rows : in_rows;

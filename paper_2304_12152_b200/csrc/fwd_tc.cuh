@@ -11,7 +11,22 @@ namespace tc {
 constexpr int C = 32;          // channels the fused kernel is built for (PRESET_PAPER)
 constexpr int M = 128;         // pixels per UMMA M-tile (one strip row)
 constexpr int NPIX = M + 2;    // A row buffer pixels: one zero pixel each side
-constexpr int PLANE = NPIX * 16;  // bytes per 8-channel K-chunk plane of a row
+// bytes per 8-channel K-chunk plane of a row: NPIX pixels rounded up to whole
+// 128-B lines so every plane of a row starts at the same bank phase
+constexpr int PLANE = (NPIX * 16 + 127) / 128 * 128;
+// A-row buffers start 16 B before a 128-B boundary, so pixel 0 of a strip row
+// (buffer pixel 1) is line aligned and a warp's 512-B store is 4 wavefronts
+constexpr int A_PHASE = 112;
+// strip geometry, identical for every pass: a strip row holds lanes
+// [STRIP_L, STRIP_L + STRIP_S) of output plus >= G halo lanes each side.
+// Pass buffers store column v at v + XPAD with a pitch that is a multiple of 8
+// pixels, so lane 0 of every strip row (v = s*STRIP_S - STRIP_L) is 128-B
+// aligned in the fp32 channel-group-planar layout.
+constexpr int STRIP_L = 4;
+constexpr int STRIP_S = M - 2 * STRIP_L;
+constexpr int XPAD = STRIP_L;
+static_assert(STRIP_S % 8 == 0, "strip stride must keep 128-B alignment");
+__host__ __device__ inline int64_t x_pitch(int VW) { return ((int64_t)VW + XPAD + 7) / 8 * 8; }
 constexpr int NSLICE = 5;      // doubled ky sequence [2,1,0,2,1] (rotation windows)
 
 // weight tile bytes for one (kx, kh) UMMA K-step: 2 K-chunks x 5*ns rows x 16 B
