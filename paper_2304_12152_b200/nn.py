@@ -291,6 +291,10 @@ class Adam:
                   flat.numel(), self.t, float(lr), self.beta1, self.beta2, self.eps,
                   _lib.stream_ptr())
 
+    def invalidate_device_state(self):
+        """Host m/v were rewritten (checkpoint load): re-upload on next step."""
+        self._dm = self._dv = None
+
     def pull_state(self):
         """Device moments -> the host lists (checkpointing / inspection)."""
         if self._dm is None:
@@ -330,3 +334,9 @@ def cosine_lr(t, total, lr_start=3e-4, lr_end=1e-5):
     if t < 0:
         raise ValueError("step must be non-negative")
     return float(lr_end + 0.5 * (lr_start - lr_end) * (1.0 + math.cos(math.pi * t / total)))
+
+
+# checkpoint format (nn.py:200-300), re-exported so `from ...nn import
+# load_checkpoint` works as it does for the reference
+from .checkpoint import (CheckpointError, load_checkpoint, network_from_checkpoint,  # noqa: E402
+                         read_checkpoint, save_checkpoint)

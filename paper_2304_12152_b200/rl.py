@@ -19,7 +19,7 @@ from . import _lib
 from .hvs import HvsConfig
 from .imagecore import Rng, gaussian_noise_map, random_crop
 from .metrics import MetricConfig, reward, reward_le_device
-from .nn import Adam, PolicyNetwork, cosine_lr
+from .nn import Adam, PolicyNetwork, cosine_lr, load_checkpoint
 from .spectral import anisotropy_device, ring_partition
 
 ESTIMATORS = ("reinforce", "reinforce_meanbaseline", "coma", "local_expectation")
@@ -239,17 +239,22 @@ def _part_cache(size):
 
 
 def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None):
-    """rl.py:281-303 (checkpoint resume is a host file format)."""
+    """rl.py:281-303.  resume_path restores parameters, Adam state, the
+    iteration counter and the RNG state words, so a split run reproduces an
+    unsplit one."""
     cfg.validate()
     if not dataset:
         raise ValueError("dataset is empty")
-    if resume_path is not None:
-        raise NotImplementedError("checkpoint resume is outside this round's scope")
     rng = Rng(cfg.seed)
     net = PolicyNetwork(channels=cfg.channels, blocks=cfg.blocks)
     adam = Adam(net.params())
     net.init_params(rng)
-    for t in range(cfg.iterations):
+    start = 0
+    if resume_path is not None:
+        meta = load_checkpoint(resume_path, net, adam)
+        start = meta["iteration"]
+        rng.set_state_words(meta["rng_state"])
+    for t in range(start, cfg.iterations):
         diag = train_step(net, adam, dataset, cfg, rng, t, group=group)
         if on_iteration is not None:
             on_iteration(t, diag, net, adam, rng)
