@@ -54,6 +54,21 @@ int ht_rng_seed(uint64_t seed, uint64_t state[4]);            /* Rng.__init__ im
 int ht_rng_uniforms(uint64_t state[4], int64_t n, double *out); /* Rng.uniforms imagecore.py:70-86 */
 int ht_rng_gaussians(uint64_t state[4], int64_t n, double *out);/* Rng.gaussians imagecore.py:88-99 */
 int ht_rng_gaussians_f32(uint64_t state[4], int64_t n, float *out);
+/* Advance state by n draws without producing them (GF(2) jump-ahead; the
+ * same stream position Rng.uniforms(n) would leave).  Not in the reference:
+ * the building block for the device streams below. */
+int ht_rng_jump(uint64_t state[4], uint64_t n);
+/* Device Rng.gaussians / Rng.uniforms: writes n values to
+ * the device buffer `out` (fp64 if f64 != 0, else fp32) on `stream`, each
+ * thread jumping to its own offset of the stream; the host state advances
+ * exactly as the host call would (uniforms: n draws; gaussians:
+ * 2*ceil(n/2)).  Uniforms are bit-exact; gaussians use the device's fp64
+ * log/sin/cos (<= 2 ulp from libm: fp32-rounded values match the host
+ * stream except for ~1e-8 of samples, by one fp32 ulp).  Replaces the
+ * host loops of gaussian_noise_map (imagecore.py:155-159) and the action
+ * uniforms of rl.sample_actions (rl.py:67-69). */
+int ht_rng_gaussians_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream);
+int ht_rng_uniforms_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream);
 
 /* ---- policy network parameters ----------------------------------------- */
 /* Number of float64 parameters of PolicyNetwork(channels, blocks, in_ch=2). */

@@ -28,6 +28,9 @@ SIGNATURES = {
     "ht_rng_uniforms": [_u64p, _i64, _vp],
     "ht_rng_gaussians": [_u64p, _i64, _vp],
     "ht_rng_gaussians_f32": [_u64p, _i64, _vp],
+    "ht_rng_jump": [_u64p, C.c_uint64],
+    "ht_rng_gaussians_device": [_u64p, _i64, _vp, _i, _vp],
+    "ht_rng_uniforms_device": [_u64p, _i64, _vp, _i, _vp],
     "ht_num_params": [_i, _i, _i64p],
     "ht_packed_bytes": [_i, _i, _i64p],
     "ht_pack_params": [_vp, _i, _i, _vp, _vp],

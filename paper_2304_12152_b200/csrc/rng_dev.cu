@@ -1,0 +1,190 @@
+// Device xoshiro256++ streams with exact jump-ahead.
+//
+// Rng.uniforms / Rng.gaussians (imagecore.py:70-99) are one sequential
+// xoshiro256++ stream.  Its state update is linear over GF(2)^256, so
+// advancing by n draws is a product of the precomputed bit matrices
+// J_k = T^(2^k) for the set bits of n.  A kernel thread jumps straight to its
+// own offset in the stream, so a noise map or action-uniform map is produced
+// on the GPU in one launch, draw-for-draw the same stream as the host; the
+// host state is then advanced by the same count (bit-exact).
+//
+// Uniforms are bit-exact.  Gaussians use the device's fp64 log / sqrt /
+// sin / cos (<= 2 ulp from the host libm), so fp64 values may differ in the
+// last bits and the fp32-rounded noise the fused kernel consumes matches the
+// host's except for ~1e-8 of samples (one fp32 ulp when it differs).
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ht {
+namespace rng {
+
+constexpr int LEVELS = 56;  // jumps of up to 2^56 draws
+
+struct Mat {
+  uint64_t col[256][4];  // column j = image of state bit j
+};
+
+__host__ __device__ __forceinline__ void transition(uint64_t s[4]) {
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = (s[3] << 45) | (s[3] >> 19);
+}
+
+static void matvec_host(const Mat &m, uint64_t s[4]) {
+  uint64_t o[4] = {0, 0, 0, 0};
+  for (int j = 0; j < 256; ++j)
+    if ((s[j >> 6] >> (j & 63)) & 1)
+      for (int w = 0; w < 4; ++w) o[w] ^= m.col[j][w];
+  for (int w = 0; w < 4; ++w) s[w] = o[w];
+}
+
+static const std::vector<Mat> &tables() {
+  static std::vector<Mat> t;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    t.resize(LEVELS);
+    for (int j = 0; j < 256; ++j) {
+      uint64_t s[4] = {0, 0, 0, 0};
+      s[j >> 6] = 1ull << (j & 63);
+      transition(s);
+      for (int w = 0; w < 4; ++w) t[0].col[j][w] = s[w];
+    }
+    for (int k = 1; k < LEVELS; ++k)
+      for (int j = 0; j < 256; ++j) {
+        uint64_t s[4];
+        for (int w = 0; w < 4; ++w) s[w] = t[k - 1].col[j][w];
+        matvec_host(t[k - 1], s);
+        for (int w = 0; w < 4; ++w) t[k].col[j][w] = s[w];
+      }
+  });
+  return t;
+}
+
+void jump_host(uint64_t s[4], uint64_t n) {
+  const auto &t = tables();
+  for (int k = 0; k < LEVELS && n; ++k, n >>= 1)
+    if (n & 1) matvec_host(t[k], s);
+}
+
+static const Mat *device_tables() {
+  static std::mutex mu;
+  static const Mat *per_dev[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!per_dev[dev]) {
+    Mat *d = nullptr;
+    if (cudaMalloc(&d, sizeof(Mat) * LEVELS) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, tables().data(), sizeof(Mat) * LEVELS, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    per_dev[dev] = d;
+  }
+  return per_dev[dev];
+}
+
+__device__ __forceinline__ void jump_dev(const Mat *__restrict__ J, uint64_t s[4], uint64_t n) {
+  for (int k = 0; k < LEVELS && n; ++k, n >>= 1) {
+    if (!(n & 1)) continue;
+    uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+    const ulonglong2 *c = reinterpret_cast<const ulonglong2 *>(J[k].col);
+#pragma unroll 4
+    for (int j = 0; j < 256; ++j) {
+      const ulonglong2 a = __ldg(c + 2 * j), b = __ldg(c + 2 * j + 1);
+      const uint64_t m = 0ull - ((s[j >> 6] >> (j & 63)) & 1ull);
+      o0 ^= a.x & m; o1 ^= a.y & m; o2 ^= b.x & m; o3 ^= b.y & m;
+    }
+    s[0] = o0; s[1] = o1; s[2] = o2; s[3] = o3;
+  }
+}
+
+__device__ __forceinline__ uint64_t next_dev(uint64_t s[4]) {
+  const uint64_t x = s[0] + s[3];
+  const uint64_t out = ((x << 23) | (x >> 41)) + s[0];
+  transition(s);
+  return out;
+}
+__device__ __forceinline__ double unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+constexpr int PAIRS_PER_THREAD = 128;
+
+// n gaussians = ceil(n/2) Box-Muller pairs; pair i consumes draws 2i, 2i+1
+template <typename T>
+__global__ void gaussians_kernel(ulonglong4 start, int64_t n, const Mat *__restrict__ J, T *__restrict__ out) {
+  const int64_t npairs = (n + 1) / 2;
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * PAIRS_PER_THREAD;
+  if (p0 >= npairs) return;
+  uint64_t s[4] = {start.x, start.y, start.z, start.w};
+  jump_dev(J, s, 2ull * (uint64_t)p0);
+  const int64_t p1 = min(npairs, p0 + PAIRS_PER_THREAD);
+  const double two_pi = 2.0 * 3.14159265358979323846;
+  for (int64_t p = p0; p < p1; ++p) {
+    const double u0 = unit(next_dev(s));
+    const double u1 = unit(next_dev(s));
+    const double r = sqrt(-2.0 * log(1.0 - u0));
+    double sn, cs;
+    sincos(two_pi * u1, &sn, &cs);
+    out[2 * p] = (T)(r * cs);
+    if (2 * p + 1 < n) out[2 * p + 1] = (T)(r * sn);
+  }
+}
+
+constexpr int DRAWS_PER_THREAD = 256;
+
+template <typename T>
+__global__ void uniforms_kernel(ulonglong4 start, int64_t n, const Mat *__restrict__ J, T *__restrict__ out) {
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * DRAWS_PER_THREAD;
+  if (i0 >= n) return;
+  uint64_t s[4] = {start.x, start.y, start.z, start.w};
+  jump_dev(J, s, (uint64_t)i0);
+  const int64_t i1 = min(n, i0 + DRAWS_PER_THREAD);
+  for (int64_t i = i0; i < i1; ++i) out[i] = (T)unit(next_dev(s));
+}
+
+template <typename T, bool GAUSS>
+static int launch(uint64_t state[4], int64_t n, T *out, cudaStream_t st) {
+  HT_REQUIRE(n >= 0, "n must be non-negative");
+  if (n == 0) return HT_OK;
+  const Mat *J = device_tables();
+  HT_REQUIRE(J != nullptr, "could not upload RNG jump tables");
+  const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
+  const int64_t units = GAUSS ? ((n + 1) / 2 + PAIRS_PER_THREAD - 1) / PAIRS_PER_THREAD
+                              : (n + DRAWS_PER_THREAD - 1) / DRAWS_PER_THREAD;
+  const int threads = 128;
+  const int64_t blocks = (units + threads - 1) / threads;
+  HT_REQUIRE(blocks < (1ll << 31), "too many draws");
+  if (GAUSS) gaussians_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(s0, n, J, out);
+  else uniforms_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(s0, n, J, out);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  jump_host(state, GAUSS ? 2ull * (uint64_t)((n + 1) / 2) : (uint64_t)n);
+  return HT_OK;
+}
+
+}  // namespace rng
+}  // namespace ht
+
+extern "C" {
+
+// Rng.jump: advance a host state by n draws (GF(2) jump-ahead).
+int ht_rng_jump(uint64_t state[4], uint64_t n) {
+  ht::rng::jump_host(state, n);
+  return HT_OK;
+}
+// Device Rng.gaussians / Rng.uniforms: out is a device pointer; the host
+// state advances exactly as the host functions would.
+int ht_rng_gaussians_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream) {
+  return f64 ? ht::rng::launch<double, true>(state, n, (double *)out, (cudaStream_t)stream)
+             : ht::rng::launch<float, true>(state, n, (float *)out, (cudaStream_t)stream);
+}
+int ht_rng_uniforms_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream) {
+  return f64 ? ht::rng::launch<double, false>(state, n, (double *)out, (cudaStream_t)stream)
+             : ht::rng::launch<float, false>(state, n, (float *)out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -79,6 +79,43 @@ class Rng:
     def gaussian(self):
         return float(self.gaussians(1)[0])
 
+    def jump(self, n):
+        """Advance the stream by n draws without producing them."""
+        _lib.call("ht_rng_jump", self._s, C.c_uint64(int(n)))
+
+    def _device_out(self, n, out, dtype, device):
+        import torch
+        if out is None:
+            dev = torch.device(device) if device is not None else torch.device(
+                "cuda", torch.cuda.current_device())
+            out = torch.empty(int(n), dtype=dtype, device=dev)
+        if not out.is_cuda or not out.is_contiguous() or out.numel() != int(n) or out.dtype not in (
+                torch.float32, torch.float64):
+            raise ValueError("out must be a contiguous CUDA float32/float64 tensor of n elements")
+        return out
+
+    def gaussians_device(self, n, out=None, dtype=None, device=None):
+        """Rng.gaussians(n) generated on the GPU (same stream; the host state
+        advances identically).  Returns a CUDA tensor (float32 by default)."""
+        import torch
+        _lib.require_cuda()
+        out = self._device_out(n, out, dtype or torch.float32, device)
+        with torch.cuda.device(out.device):
+            _lib.call("ht_rng_gaussians_device", self._s, C.c_int64(int(n)), _lib.ptr(out),
+                      int(out.dtype == torch.float64), _lib.stream_ptr())
+        return out
+
+    def uniforms_device(self, n, out=None, dtype=None, device=None):
+        """Rng.uniforms(n) generated on the GPU (bit-exact; the host state
+        advances identically).  Returns a CUDA tensor (float64 by default)."""
+        import torch
+        _lib.require_cuda()
+        out = self._device_out(n, out, dtype or torch.float64, device)
+        with torch.cuda.device(out.device):
+            _lib.call("ht_rng_uniforms_device", self._s, C.c_int64(int(n)), _lib.ptr(out),
+                      int(out.dtype == torch.float64), _lib.stream_ptr())
+        return out
+
     def randint(self, n):
         """imagecore.py:104-108."""
         if n <= 0:
@@ -109,6 +146,14 @@ def gaussian_noise_map_f32(rng, width, height):
     if width <= 0 or height <= 0:
         raise ValueError("noise map dimensions must be positive")
     return rng.gaussians_f32(width * height).reshape(height, width)
+
+
+def gaussian_noise_map_device(rng, width, height, dtype=None, device=None):
+    """gaussian_noise_map drawn on the GPU: (height, width) CUDA tensor
+    (float32 by default, the fused kernel's input type)."""
+    if width <= 0 or height <= 0:
+        raise ValueError("noise map dimensions must be positive")
+    return rng.gaussians_device(width * height, dtype=dtype, device=device).view(height, width)
 
 
 def constant_image(gray, width, height):
