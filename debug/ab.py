@@ -14,8 +14,11 @@ batch = sys.argv[sys.argv.index('--batch') + 1] if '--batch' in sys.argv else '6
 res = {l: [] for l in libs}
 for _ in range(reps):
     for l in libs:
-        out = subprocess.run([sys.executable, 'debug/passtime.py', batch, 'x'], capture_output=True, text=True,
-                             env={**os.environ, 'HTB200_LIB': l}, timeout=300).stdout.strip().splitlines()[-1]
+        pr = subprocess.run([sys.executable, 'debug/passtime.py', batch, 'x'], capture_output=True, text=True,
+                            env={**os.environ, 'HTB200_LIB': l}, timeout=300)
+        if pr.returncode != 0:
+            sys.exit(f"{l}: passtime failed\n{pr.stderr[-2000:]}")
+        out = pr.stdout.strip().splitlines()[-1]
         d = eval(out.split(' ', 1)[1])
         res[l].append(d)
 for l in libs:
