@@ -106,6 +106,15 @@ int ht_halftone(const void *packed_dev, int channels, int blocks,
                 float *p_dev, uint8_t *h_dev, uint8_t *pbm_dev,
                 void *workspace_dev, int64_t workspace_bytes, int impl,
                 void *stream);
+/* Multitone inference (multitone.infer_multitone / quantize_multitone,
+ * multitone.py:61-76): same forward as ht_halftone, the
+ * epilogue writes q_dev = index of the nearest level i/(levels-1) of p
+ * (half-steps round up) as uint8; levels in [2, 256] (2 = ht_halftone's h). */
+int ht_multitone(const void *packed_dev, int channels, int blocks,
+                 const float *c_dev, const float *z_dev, int B, int H, int W,
+                 int in_row0, int in_rows, int out_row0, int out_rows, int levels,
+                 float *p_dev, uint8_t *q_dev, void *workspace_dev,
+                 int64_t workspace_bytes, int impl, void *stream);
 /* Reads the non-finite-logit flag the last ht_halftone left in `workspace_dev`
  * (synchronises `stream`); HT_E_NONFINITE if set (nn.py:147-148). */
 int ht_halftone_check(const void *workspace_dev, void *stream);
@@ -155,6 +164,31 @@ int ht_reward_le(const float *p_dev, const double *u_dev, const float *c_dev,
                  float *signal_out_dev, double *reward_out_dev,
                  void *workspace_dev, int64_t workspace_bytes, void *stream);
 int ht_reward_workspace_bytes(int B, int H, int W, int64_t *bytes);
+/* General form (L output levels, estimators):
+ *   u_dev != NULL: actions sampled by the two-point cast of p onto the
+ *     lattice i/(L-1) (rl._cast_two_point / _sample_two_point, rl.py:40-69);
+ *   u_dev == NULL: p_dev holds the action map itself (RewardContext).
+ *   estimator 0: local expectation, (m == ceil ? D : -D) * (L-1)
+ *              (rl.le_signal, rl.py:96-109; multitone_le, multitone.py:56-59)
+ *   estimator 1: COMA (rl.coma_signal, rl.py:117-129), L = 2 only
+ *   estimator 2: raw delta D(a -> other[a]) (metrics.delta_map, needs
+ *              other_dev: (B,H,W) float32 substitute values)
+ * where D is the reward change of moving pixel a to the other support point
+ * (or to other[a]).  signal_out = signal * scale.  ht_reward_le is this
+ * entry with L = 2, estimator 0. */
+int ht_reward_signal(const float *p_dev, const double *u_dev, const float *other_dev,
+                     const float *c_dev, int B, int H, int W, const double *k_hvs_dev,
+                     int ksize, const double *w_ssim_dev, int wsize, double w_s, double c1,
+                     double c2, double gain, int levels, int estimator, double scale,
+                     float *m_out_dev, float *signal_out_dev, double *reward_out_dev,
+                     void *workspace_dev, int64_t workspace_bytes, void *stream);
+/* REINFORCE / REINFORCE with mean baseline (rl.reinforce_signal,
+ * rl.py:132-136): signal = -dlogpi(p, m) (reward[b] - baseline) * scale,
+ * dlogpi = 1/q (m = 1) or -1/(1-q) (m = 0), q = clip(p, 1e-7, 1 - 1e-7);
+ * p, m, signal (B, n) float32, reward (B) float64. */
+int ht_reinforce_signal(const float *p_dev, const float *m_dev, int B, int64_t n,
+                        const double *reward_dev, double baseline, double scale,
+                        float *signal_out_dev, void *stream);
 
 /* ---- K5 / K7: spectral ---------------------------------------------------
  * anisotropy_loss / anisotropy_loss_backward (spectral.py:100-133) for B

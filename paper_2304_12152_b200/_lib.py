@@ -38,6 +38,8 @@ SIGNATURES = {
     "ht_halftone": [_vp, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp,
                     _i64, _i, _vp],
     "ht_halftone_check": [_vp, _vp],
+    "ht_multitone": [_vp, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i64,
+                     _i, _vp],
     "ht_last_launch_count": [_ip],
     "ht_timing_enable": [_i],
     "ht_timing_read": [_vp, _vp, _i, _ip],
@@ -47,6 +49,9 @@ SIGNATURES = {
     "ht_reward_workspace_bytes": [_i, _i, _i, _i64p],
     "ht_reward_le": [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _d, _d, _d, _d, _d, _vp, _vp,
                      _vp, _vp, _i64, _vp],
+    "ht_reward_signal": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _d, _d, _d, _d, _i, _i,
+                         _d, _vp, _vp, _vp, _vp, _i64, _vp],
+    "ht_reinforce_signal": [_vp, _vp, _i, _i64, _vp, _d, _d, _vp, _vp],
     "ht_spectral_workspace_bytes": [_i, _i, _i, _i, _i64p],
     "ht_anisotropy": [_vp, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp, _i64, _vp],
     "ht_rapsd": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _vp],

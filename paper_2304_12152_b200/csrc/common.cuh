@@ -84,4 +84,14 @@ PackLayout pack_layout(int C, int NB);
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
+// Output level of a logit on the lattice i/steps (multitone.quantize_multitone,
+// multitone.py:61-67: nearest level, half-steps round up).  steps = 1 is the
+// binary rule h = (p >= 0.5) = (logit >= 0) of rl.infer_halftone (rl.py:311).
+__device__ __forceinline__ uint8_t level_of(float logit, int steps) {
+  if (steps == 1) return logit >= 0.f ? 1 : 0;
+  const float v = 1.f / (1.f + expf(-logit));
+  const float q = floorf(v * (float)steps + 0.5f);
+  return (uint8_t)fminf(fmaxf(q, 0.f), (float)steps);
+}
+
 }  // namespace ht

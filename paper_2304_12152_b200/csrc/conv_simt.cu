@@ -195,7 +195,7 @@ __global__ void dlogit_kernel(const float *__restrict__ dp, const float *__restr
 __global__ void threshold_window_kernel(const float *__restrict__ logit, int B, int in_rows,
                                         int W, int row_off, int out_rows,
                                         float *__restrict__ p, uint8_t *__restrict__ h,
-                                        int *__restrict__ nonfinite) {
+                                        int *__restrict__ nonfinite, int steps) {
   const int64_t n = (int64_t)B * out_rows * W;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -205,7 +205,7 @@ __global__ void threshold_window_kernel(const float *__restrict__ logit, int B, 
   const float l = logit[((int64_t)b * in_rows + y + row_off) * W + xx];
   if (!isfinite(l)) atomicOr(nonfinite, 1);
   if (p) p[i] = 1.f / (1.f + expf(-l));
-  if (h) h[i] = l >= 0.f ? 1 : 0;
+  if (h) h[i] = level_of(l, steps);
 }
 
 }  // namespace ht
@@ -298,7 +298,7 @@ static int simt_forward(const void *packed, int C, int NB, const float *x, int B
 int simt_halftone(const void *packed, int C, int NB, const float *c, const float *z, int B,
                   int H, int W, int in_row0, int in_rows, int out_row0, int out_rows,
                   float *p, uint8_t *h, void *ws, int64_t ws_bytes, int *nonfinite_dev,
-                  cudaStream_t st) {
+                  int levels, cudaStream_t st) {
   const size_t plane = (size_t)in_rows * W;
   const size_t act = (size_t)B * C * plane;
   const int64_t need = (int64_t)sizeof(float) * (3 * act + (size_t)B * 2 * plane + (size_t)B * plane);
@@ -318,7 +318,7 @@ int simt_halftone(const void *packed, int C, int NB, const float *c, const float
   if (rc) return rc;
   const int64_t n = (int64_t)B * out_rows * W;
   threshold_window_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      logits, B, in_rows, W, out_row0 - in_row0, out_rows, p, h, nonfinite_dev);
+      logits, B, in_rows, W, out_row0 - in_row0, out_rows, p, h, nonfinite_dev, levels - 1);
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;

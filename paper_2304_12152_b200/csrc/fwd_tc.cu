@@ -334,6 +334,7 @@ struct TcParams {
   long long chunk;      // strip-rows per CTA: CTA i owns [i*chunk, (i+1)*chunk) of
                         // the strip-major (strip, row) space, split into segments
   int out_rows;         // HO: rows of p/h (== r_hi - r_lo)
+  int steps;            // HO: output lattice i/steps (1 = binary halftone)
 };
 
 // Biases live in the constant bank (not SMEM: the tensor core's operand reads
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
               if (!isfinite(logit)) atomicOr(P.flag, 1);
               const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
               if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
-              if (P.h) P.h[o] = logit >= 0.f ? 1 : 0;
+              if (P.h) P.h[o] = level_of(logit, P.steps);
             }
           } else if constexpr (PL::feeds_next(j)) {
             const int q = NABUF == 3 ? slot : (d & 1);   // A buffer of row d
@@ -878,7 +879,7 @@ static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
 
 int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float *z, int B, int H,
         int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p, uint8_t *h,
-        void *ws, int64_t ws_bytes, int *flag_dev, cudaStream_t st) {
+        void *ws, int64_t ws_bytes, int *flag_dev, int levels, cudaStream_t st) {
   (void)H;
   const int64_t need = workspace_bytes(NB, B, H, W, in_rows);
   HT_REQUIRE(ws_bytes >= need, "workspace too small: %lld < %lld", (long long)ws_bytes, (long long)need);
@@ -923,6 +924,7 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     prm.r_lo = pd.ho ? out_row0 - in_row0 : 0;
     prm.r_hi = pd.ho ? out_row0 - in_row0 + out_rows : in_rows;
     prm.out_rows = out_rows;
+    prm.steps = levels - 1;
     // balanced split of the strip-major (strip, row) space over the SMs; each
     // CTA gets >= 8G rows so halo recompute stays small
     const long long total = (long long)prm.n_strips * (prm.r_hi - prm.r_lo);

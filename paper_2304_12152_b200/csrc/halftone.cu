@@ -7,7 +7,8 @@
 namespace ht {
 int simt_halftone(const void *packed, int C, int NB, const float *c, const float *z, int B,
                   int H, int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p,
-                  uint8_t *h, void *ws, int64_t ws_bytes, int *nonfinite_dev, cudaStream_t st);
+                  uint8_t *h, void *ws, int64_t ws_bytes, int *nonfinite_dev, int levels,
+                  cudaStream_t st);
 int64_t simt_halftone_ws(int C, int B, int W, int in_rows);
 
 // PBM P4 payload from a uint8 halftone (1 = white): bit = 1 - h, MSB first,
@@ -47,15 +48,20 @@ int ht_halftone_workspace_bytes(int C, int NB, int B, int H, int W, int in_rows,
   return HT_OK;
 }
 
-int ht_halftone(const void *packed, int C, int NB, const float *c, const float *z, int B, int H,
+}  // extern "C"
+
+static int halftone_impl(const void *packed, int C, int NB, const float *c, const float *z, int B, int H,
                 int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p,
-                uint8_t *h, uint8_t *pbm, void *ws, int64_t ws_bytes, int impl, void *stream) {
+                uint8_t *h, uint8_t *pbm, void *ws, int64_t ws_bytes, int impl, int levels,
+                void *stream) {
   ht::reset_launches();
   HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "input must be non-empty (B=%d H=%d W=%d)", B, H, W);
   HT_REQUIRE(in_row0 >= 0 && in_rows >= 1 && in_row0 + in_rows <= H, "bad input row window");
   HT_REQUIRE(out_row0 >= in_row0 && out_rows >= 1 && out_row0 + out_rows <= in_row0 + in_rows,
              "output rows must lie inside the input rows");
   HT_REQUIRE(impl == 0 || impl == 1, "impl must be 0 (tensor core) or 1 (simt)");
+  HT_REQUIRE(levels >= 2 && levels <= 256, "levels must be in [2, 256]");
+  HT_REQUIRE(levels == 2 || pbm == nullptr, "the PBM payload is binary (levels = 2)");
   if (impl == 0 && C != ht::tc::C)
     return ht::fail(HT_E_UNSUPPORTED, "fused tensor-core forward is built for channels=%d (got %d)",
                     ht::tc::C, C);
@@ -76,10 +82,10 @@ int ht_halftone(const void *packed, int C, int NB, const float *c, const float *
     ht::PackLayout L = ht::pack_layout(C, NB);
     rc = ht::tc::run((const char *)packed + L.tc_off, (const float *)((const char *)packed + L.tcb_off),
                      NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p, hout, rest,
-                     rest_bytes, flag, st);
+                     rest_bytes, flag, levels, st);
   } else {
     rc = ht::simt_halftone(packed, C, NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p,
-                           hout, rest, rest_bytes, flag, st);
+                           hout, rest, rest_bytes, flag, levels, st);
   }
   if (rc) return rc;
   if (pbm) {
@@ -90,6 +96,24 @@ int ht_halftone(const void *packed, int C, int NB, const float *c, const float *
     HT_CHECK_LAUNCH();
   }
   return HT_OK;
+}
+
+extern "C" {
+
+int ht_halftone(const void *packed, int C, int NB, const float *c, const float *z, int B, int H,
+                int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p,
+                uint8_t *h, uint8_t *pbm, void *ws, int64_t ws_bytes, int impl, void *stream) {
+  return halftone_impl(packed, C, NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p, h,
+                       pbm, ws, ws_bytes, impl, 2, stream);
+}
+
+// Multitone inference (multitone.infer_multitone, multitone.py:70-76): q =
+// index of the nearest level i/(levels-1) (half-steps round up), uint8.
+int ht_multitone(const void *packed, int C, int NB, const float *c, const float *z, int B, int H,
+                 int W, int in_row0, int in_rows, int out_row0, int out_rows, int levels, float *p,
+                 uint8_t *q, void *ws, int64_t ws_bytes, int impl, void *stream) {
+  return halftone_impl(packed, C, NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p, q,
+                       nullptr, ws, ws_bytes, impl, levels, stream);
 }
 
 // Non-finite flag of the last ht_halftone that used `ws` (reads 4 bytes;

@@ -2,15 +2,22 @@
 // flip-reward signal, fp64 math (the training signal is ~1e-5 and must stay
 // within 1e-4 relative of the reference).
 //
-// Reference (region="full", binary policy L=2):
-//   sampling      m = (u < p)                          rl.py:67-69
+// Reference (region="full"; L output levels i/(L-1), L=2 the binary policy):
+//   sampling      two-point cast of p onto the lattice (floor, ceil, p_ceil =
+//                 frac) and m = u < p_ceil ? ceil : floor   rl.py:40-69
+//                 (L=2: m = (u < p) bit for bit)
 //   RewardContext f = conv(., k) (true convolution), window sums mu/E[..]
 //                 by correlation with the SSIM window w; sigma_c, SSIM,
 //                 CSSIM, reward map, scalar R         metrics.py:165-204, 95-107
 //   delta_map     dSSE = 2 d corr(e,k) + d^2 corr(1,k^2); dCS summed over the
 //                 window positions b covering a        metrics.py:333-392
-//   le_signal     signal = -sign * delta, sign = -1 where m = 1   rl.py:96-109
-// Since m is binary, E[h^2] = mu_h exactly (metrics.py:193 on a 0/1 map).
+//   estimators    per pixel from the flip delta D (moving pixel a to the other
+//                 support point):
+//                 local expectation  (m == ceil ? D : -D) * (L-1)    rl.py:96-109
+//                 COMA (L=2)         h=1: (1-q) D / q, h=0: -q D / (1-q),
+//                                    q = clip(p, 1e-7, 1-1e-7)      rl.py:117-129
+//                 REINFORCE variants use the per-image reward only
+//                 (ht_reinforce_signal)                             rl.py:132-136
 #include "common.cuh"
 
 namespace ht {
@@ -33,15 +40,26 @@ __device__ __forceinline__ double ssim3(double mx, double my, double sxx, double
   return lum * con * str;
 }
 
+constexpr int NMAPS = 8;
+
+// two-point cast (rl.py:40-57): floor / ceil lattice values and upper mass
+__device__ __forceinline__ void cast_two_point(double v, int steps, double &fl, double &ce, double &frac) {
+  const double scaled = v * steps;
+  const double idx = floor(scaled);
+  frac = scaled - idx;
+  fl = idx / steps;
+  ce = frac == 0.0 ? fl : fmin(idx + 1.0, (double)steps) / steps;
+}
+
 // Stage 1: per pixel maps.  Workspace layout per image (doubles, n = H*W):
-//   [0] e  [1] mu_h  [2] shc  [3] mu_c  [4] scc  [5] sigma_c  [6] ssim
+//   [0] e  [1] mu_h  [2] shc  [3] mu_c  [4] scc  [5] sigma_c  [6] ssim  [7] shh
 // plus per-image sums[2] = {sum e^2, sum cssim}.  Also writes m.
 __global__ void __launch_bounds__(256)
 reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
                    const float *__restrict__ c, int H, int W, const double *__restrict__ k,
                    int ks, const double *__restrict__ w, int wsz, double c1, double c2,
-                   double gain, double w_s, float *__restrict__ m_out, double *__restrict__ maps,
-                   double *__restrict__ sums) {
+                   double gain, double w_s, int steps, float *__restrict__ m_out,
+                   double *__restrict__ maps, double *__restrict__ sums) {
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
   const int hk = ks / 2, hw = wsz / 2, hh = hk > hw ? hk : hw;
@@ -62,7 +80,13 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
     double mv = 0.0, cv = 0.0;
     if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
       const size_t idx = (size_t)gy * W + gx;
-      mv = ub[idx] < (double)pb[idx] ? 1.0 : 0.0;
+      if (ub) {
+        double fl, ce, frac;
+        cast_two_point((double)pb[idx], steps, fl, ce, frac);
+        mv = ub[idx] < frac ? ce : fl;
+      } else {
+        mv = (double)pb[idx];                 // action map given (RewardContext)
+      }
       cv = (double)cb[idx];
     }
     sm[yy][xx] = mv;
@@ -83,22 +107,23 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
         fc += kv * sc[yy][xx];
       }
     // window sums by correlation with w
-    double muh = 0.0, shc = 0.0, muc = 0.0, scc = 0.0;
+    double muh = 0.0, shc = 0.0, muc = 0.0, scc = 0.0, shh = 0.0;
     for (int i = 0; i < wsz; ++i)
       for (int j = 0; j < wsz; ++j) {
         const double wv = sw[i * wsz + j];
         const int yy = ty + RH + i - hw, xx = tx + RH + j - hw;
         const double mv = sm[yy][xx], cv = sc[yy][xx];
         muh += wv * mv;
+        shh += wv * (mv * mv);
         shc += wv * (mv * cv);
         muc += wv * cv;
         scc += wv * (cv * cv);
       }
     const double sig = fmin(gain * sqrt(fmax(scc - muc * muc, 0.0)), 1.0);
-    const double s = ssim3(muh, muc, muh, scc, shc, c1, c2);
+    const double s = ssim3(muh, muc, shh, scc, shc, c1, c2);
     const double e = fh - fc;
     const size_t idx = (size_t)gy * W + gx;
-    double *mb = maps + (size_t)b * 7 * n;
+    double *mb = maps + (size_t)b * NMAPS * n;
     mb[0 * n + idx] = e;
     mb[1 * n + idx] = muh;
     mb[2 * n + idx] = shc;
@@ -106,6 +131,7 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
     mb[4 * n + idx] = scc;
     mb[5 * n + idx] = sig;
     mb[6 * n + idx] = s;
+    mb[7 * n + idx] = shh;
     m_out[b * n + idx] = (float)sm[ty + RH][tx + RH];
     e2 = e * e;
     cs = sig * s + (1.0 - sig);
@@ -128,21 +154,23 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
   }
 }
 
-// Stage 2: delta for flipping every pixel, LE signal (scaled), per pixel a.
+// Stage 2: delta for moving every pixel to its other support point, then
+// the estimator's signal (scaled), per pixel a.  estimator: 0 = local
+// expectation, 1 = COMA (binary only).
 __global__ void __launch_bounds__(256)
-reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ c, int H, int W,
-                 const double *__restrict__ k, int ks, const double *__restrict__ w, int wsz,
-                 double c1, double c2, double w_s, double scale, const double *__restrict__ maps,
-                 float *__restrict__ signal) {
+reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ p, const float *__restrict__ other,
+                 const float *__restrict__ c, int H, int W, const double *__restrict__ k, int ks, const double *__restrict__ w, int wsz,
+                 double c1, double c2, double w_s, double scale, int steps, int estimator,
+                 const double *__restrict__ maps, float *__restrict__ signal) {
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
   const int hk = ks / 2, hw = wsz / 2;
   constexpr int TP = RT + 2 * RH;
-  // b-side maps around the tile: e, mu_h, shc, mu_c, scc, sigma_c, ssim
-  __shared__ double sb[7][TP][TP];
+  // b-side maps around the tile: e, mu_h, shc, mu_c, scc, sigma_c, ssim, shh
+  __shared__ double sb[NMAPS][TP][TP];
   __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
   const size_t n = (size_t)H * W;
-  const double *mb = maps + (size_t)b * 7 * n;
+  const double *mb = maps + (size_t)b * NMAPS * n;
   for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
   for (int i = threadIdx.x; i < wsz * wsz; i += 256) sw[i] = w[i];
   for (int i = threadIdx.x; i < TP * TP; i += 256) {
@@ -151,16 +179,26 @@ reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ c, in
     const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
     const size_t idx = in ? (size_t)gy * W + gx : 0;
 #pragma unroll
-    for (int q = 0; q < 7; ++q) sb[q][yy][xx] = in ? mb[q * n + idx] : 0.0;
+    for (int q = 0; q < NMAPS; ++q) sb[q][yy][xx] = in ? mb[q * n + idx] : 0.0;
   }
   __syncthreads();
   const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
   const int gy = y0 + ty, gx = x0 + tx;
   if (gy >= H || gx >= W) return;
   const size_t ia = (size_t)gy * W + gx;
-  const double ma = (double)m_in[b * n + ia];
+  const float mf = m_in[b * n + ia];
+  double ma = (double)mf;
   const double ca = (double)c[b * n + ia];
-  const double d = 1.0 - 2.0 * ma;  // other - h for a flip (+-1)
+  // other support point (rl.py:98-99): m == ceil ? floor : ceil
+  const double pa = (double)p[b * n + ia];
+  double lv, hv, frac;
+  cast_two_point(pa, steps, lv, hv, frac);
+  // m_out is float32: recover the exact lattice value of a sampled action
+  const bool at_ceil = mf == (float)hv;
+  if (!other) ma = at_ceil ? hv : lv;
+  // other - h: the given substitution, or the other support point (+-1 for
+  // L=2; 0 where the support collapsed)
+  const double d = other ? (double)other[b * n + ia] - ma : (at_ceil ? lv : hv) - ma;
   // dSSE = 2 d corr(e, k)[a] + d^2 sum_{y in image} k[y - a + hk]^2
   double ce = 0.0, k2 = 0.0;
   for (int i = 0; i < ks; ++i) {
@@ -190,15 +228,35 @@ reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ c, in
         const int sy = ty + RH - dy, sx = tx + RH - dx;
         const double muh = sb[1][sy][sx], shc = sb[2][sy][sx], muc = sb[3][sy][sx];
         const double scc = sb[4][sy][sx], sig = sb[5][sy][sx], s0 = sb[6][sy][sx];
-        const double s1 = ssim3(muh + wd * d, muc, muh + wd * dh, scc, shc + wd * d * ca, c1, c2);
+        const double shh = sb[7][sy][sx];
+        const double s1 = ssim3(muh + wd * d, muc, shh + wd * dh, scc, shc + wd * d * ca, c1, c2);
         dcs += sig * (s1 - s0);
       }
     }
   }
   const double delta = (-dsse + w_s * dcs) / (double)n;
-  // le_signal: -(sign * delta), sign = -1 where m == 1
-  const double sigv = ma == 1.0 ? delta : -delta;
+  double sigv;
+  if (estimator == 2) {
+    sigv = delta;                              // raw delta map (metrics.delta_map)
+  } else if (estimator == 1) {
+    // COMA: -dlogpi(p, h) (R - baseline), baseline = q R_up + (1-q) R_down
+    const double q = fmin(fmax(pa, 1e-7), 1.0 - 1e-7);
+    sigv = ma == 1.0 ? (1.0 - q) * delta / q : -q * delta / (1.0 - q);
+  } else {
+    // local expectation: -(sign * delta) / (1/(L-1)), sign = -1 where m == ceil
+    sigv = (at_ceil ? delta : -delta) * (double)steps;
+  }
   signal[b * n + ia] = (float)(sigv * scale);
+}
+
+__global__ void reinforce_kernel(const float *__restrict__ p, const float *__restrict__ m, int64_t total,
+                                 int64_t n, const double *__restrict__ reward, double baseline, double scale,
+                                 float *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const double q = fmin(fmax((double)p[i], 1e-7), 1.0 - 1e-7);
+    const double dl = m[i] == 1.0f ? 1.0 / q : -1.0 / (1.0 - q);
+    out[i] = (float)(-dl * (reward[i / n] - baseline) * scale);
+  }
 }
 
 __global__ void reward_finalize_kernel(const double *__restrict__ sums, int B, double n,
@@ -215,32 +273,39 @@ __global__ void reward_finalize_kernel(const double *__restrict__ sums, int B, d
 extern "C" {
 
 int ht_reward_workspace_bytes(int B, int H, int W, int64_t *bytes) {
-  *bytes = (int64_t)sizeof(double) * ((int64_t)B * 7 * H * W + 2 * (int64_t)B) + 256;
+  *bytes = (int64_t)sizeof(double) * ((int64_t)B * ht::NMAPS * H * W + 2 * (int64_t)B) + 256;
   return HT_OK;
 }
 
-int ht_reward_le(const float *p, const double *u, const float *c, int B, int H, int W,
-                 const double *k, int ks, const double *w, int wsz, double w_s, double c1,
-                 double c2, double gain, double scale, float *m_out, float *signal_out,
-                 double *reward_out, void *ws, int64_t ws_bytes, void *stream) {
+int ht_reward_signal(const float *p, const double *u, const float *other, const float *c, int B, int H, int W,
+                     const double *k, int ks, const double *w, int wsz, double w_s, double c1,
+                     double c2, double gain, int levels, int estimator, double scale, float *m_out,
+                     float *signal_out, double *reward_out, void *ws, int64_t ws_bytes, void *stream) {
   HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty batch");
   HT_REQUIRE(ks % 2 == 1 && ks <= ht::RMAXK && wsz % 2 == 1 && wsz <= ht::RMAXK,
              "stencils must be odd and at most %d wide", ht::RMAXK);
+  HT_REQUIRE(levels >= 2 && levels <= 256, "levels must be in [2, 256]");
+  HT_REQUIRE(estimator == 0 || (estimator == 1 && levels == 2) || (estimator == 2 && other != nullptr),
+             "estimator must be 0 (local expectation), 1 (COMA, binary policies only) or 2 "
+             "(delta map, needs `other`)");
+  HT_REQUIRE(u != nullptr || estimator == 2 || signal_out == nullptr,
+             "estimator signals need sampled actions (u)");
+  HT_REQUIRE(m_out != nullptr, "m_out is required");
   int64_t need = 0;
   ht_reward_workspace_bytes(B, H, W, &need);
   HT_REQUIRE(ws_bytes >= need, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   double *maps = (double *)ws;
-  double *sums = maps + (size_t)B * 7 * H * W;
+  double *sums = maps + (size_t)B * ht::NMAPS * H * W;
   HT_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 2 * B, st));
   dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
-  ht::reward_maps_kernel<<<grid, 256, 0, st>>>(p, u, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s,
+  ht::reward_maps_kernel<<<grid, 256, 0, st>>>(p, u, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s, levels - 1,
                                                m_out, maps, sums);
   ht::count_launch();
   HT_CHECK_LAUNCH();
   if (signal_out) {
-    ht::reward_le_kernel<<<grid, 256, 0, st>>>(m_out, c, H, W, k, ks, w, wsz, c1, c2, w_s, scale,
-                                                maps, signal_out);
+    ht::reward_le_kernel<<<grid, 256, 0, st>>>(m_out, p, other, c, H, W, k, ks, w, wsz, c1, c2, w_s, scale, levels - 1,
+                                                estimator, maps, signal_out);
     ht::count_launch();
     HT_CHECK_LAUNCH();
   }
@@ -250,6 +315,28 @@ int ht_reward_le(const float *p, const double *u, const float *c, int B, int H, 
     ht::count_launch();
     HT_CHECK_LAUNCH();
   }
+  return HT_OK;
+}
+
+int ht_reward_le(const float *p, const double *u, const float *c, int B, int H, int W,
+                 const double *k, int ks, const double *w, int wsz, double w_s, double c1,
+                 double c2, double gain, double scale, float *m_out, float *signal_out,
+                 double *reward_out, void *ws, int64_t ws_bytes, void *stream) {
+  return ht_reward_signal(p, u, nullptr, c, B, H, W, k, ks, w, wsz, w_s, c1, c2, gain, 2, 0, scale, m_out,
+                          signal_out, reward_out, ws, ws_bytes, stream);
+}
+
+// REINFORCE (rl.py:132-136): signal = -dlogpi(p, h) (R_b - baseline) * scale,
+// dlogpi = 1/q where h = 1, -1/(1-q) where h = 0, q = clip(p, 1e-7, 1-1e-7).
+int ht_reinforce_signal(const float *p, const float *m, int B, int64_t n, const double *reward,
+                        double baseline, double scale, float *signal_out, void *stream) {
+  HT_REQUIRE(B >= 1 && n >= 1, "empty batch");
+  const int64_t total = (int64_t)B * n;
+  const int grid = (int)((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
+  ht::reinforce_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p, m, total, n, reward, baseline, scale,
+                                                                 signal_out);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
   return HT_OK;
 }
 

@@ -53,11 +53,17 @@ def stencils_device(cfg, device):
     return _dev_cache[key]
 
 
-def reward_le_device(p, u, c, cfg, scale=1.0, want_signal=True):
-    """Batched K3+K4 on device tensors.
+ESTIMATOR_CODES = {"local_expectation": 0, "coma": 1, "delta": 2}
 
-    p, c: (B, H, W) float32; u: (B, H, W) float64 uniforms.  Returns
-    (m float32, signal float32 = le_signal * scale or None, reward float64 (B,))."""
+
+def reward_signal_device(p, u, c, cfg, scale=1.0, want_signal=True, levels=2,
+                         estimator="local_expectation", other=None):
+    """Batched K3+K4 on device tensors (ht_reward_signal).
+
+    p, c: (B, H, W) float32; u: (B, H, W) float64 uniforms, or None when p is
+    already the action map; other: (B, H, W) float32 substitutes for
+    estimator="delta".  Returns (m float32, signal float32 * scale or None,
+    reward float64 (B,))."""
     import torch
     B, H, W = p.shape
     dev = p.device
@@ -67,22 +73,41 @@ def reward_le_device(p, u, c, cfg, scale=1.0, want_signal=True):
     rew = torch.empty(B, dtype=torch.float64, device=dev)
     nbytes = _lib.out_i64("ht_reward_workspace_bytes", B, H, W)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    _lib.call("ht_reward_le", _lib.ptr(p.contiguous()), _lib.ptr(u.contiguous()),
+    _lib.call("ht_reward_signal", _lib.ptr(p.contiguous()),
+              _lib.ptr(u.contiguous()) if u is not None else None,
+              _lib.ptr(other.contiguous()) if other is not None else None,
               _lib.ptr(c.contiguous()), B, H, W, _lib.ptr(k), k.shape[0], _lib.ptr(w),
               w.shape[0], float(cfg.w_s), float(cfg.c1), float(cfg.c2), float(cfg.contrast_gain),
-              float(scale), _lib.ptr(m), _lib.ptr(sig), _lib.ptr(rew), _lib.ptr(ws), nbytes,
-              _lib.stream_ptr())
+              int(levels), ESTIMATOR_CODES[estimator], float(scale), _lib.ptr(m), _lib.ptr(sig),
+              _lib.ptr(rew), _lib.ptr(ws), nbytes, _lib.stream_ptr())
     return m, sig, rew
 
 
-class RewardContext:
-    """metrics.RewardContext for region='full' and a binary halftone h.
+def reward_le_device(p, u, c, cfg, scale=1.0, want_signal=True):
+    """Binary local-expectation form of reward_signal_device (ht_reward_le)."""
+    return reward_signal_device(p, u, c, cfg, scale, want_signal)
 
-    .reward is the scalar R = -HVS-MSE + w_s * CSSIM (metrics.py:201-203);
-    flip deltas come from delta_map()."""
+
+def reinforce_signal_device(p, m, reward_b, baseline, scale=1.0):
+    """REINFORCE signal on device tensors (ht_reinforce_signal): p, m (B,H,W)
+    float32, reward_b (B,) float64."""
+    import torch
+    B = p.shape[0]
+    out = torch.empty_like(p)
+    _lib.call("ht_reinforce_signal", _lib.ptr(p.contiguous()), _lib.ptr(m.contiguous()), B,
+              p[0].numel(), _lib.ptr(reward_b.contiguous()), float(baseline), float(scale),
+              _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+class RewardContext:
+    """metrics.RewardContext for region='full' (metrics.py:165-204).
+
+    h is any action map (binary or on an L-level lattice).  .reward is the
+    scalar R = -HVS-MSE + w_s * CSSIM (metrics.py:201-203); delta_map()
+    evaluates substitutions on the GPU (K3 maps + K4 deltas)."""
 
     def __init__(self, h, c, cfg, region="full"):
-        import torch
         if region != "full":
             if region == "valid":
                 raise NotImplementedError("region='valid' is an evaluation metric outside the "
@@ -93,21 +118,26 @@ class RewardContext:
         self.c = np.asarray(c, dtype=np.float64)
         if self.c.shape != self.h.shape:
             raise ValueError("halftone and contone shapes differ")
-        if not np.all((self.h == 0.0) | (self.h == 1.0)):
-            raise NotImplementedError("the GPU reward path handles binary halftones (L=2)")
-        _lib.require_cuda()
-        dev = torch.device("cuda", torch.cuda.current_device())
         hh, ww = self.h.shape
         self.n_region = hh * ww
-        pd = torch.from_numpy(self.h.astype(np.float32))[None].to(dev)
-        ud = torch.full((1, hh, ww), 0.5, dtype=torch.float64, device=dev)
-        cd = torch.from_numpy(self.c.astype(np.float32))[None].to(dev)
-        _, sig, rew = reward_le_device(pd, ud, cd, cfg, 1.0, True)
-        s = sig[0].double().cpu().numpy()
-        # le_signal = -sign * delta (sign = -1 where h == 1) -> flip delta
-        self._flip_delta = np.where(self.h == 1.0, s, -s)
+        _, _, rew = reward_signal_device(*self._dev(), self.cfg, want_signal=False)
         self.reward = float(rew[0].item())
         self.eval_count = 1
+
+    def _dev(self):
+        import torch
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        hd = torch.from_numpy(self.h.astype(np.float32))[None].to(dev)
+        cd = torch.from_numpy(self.c.astype(np.float32))[None].to(dev)
+        return hd, None, cd
+
+    def delta(self, other):
+        import torch
+        hd, _, cd = self._dev()
+        od = torch.from_numpy(np.asarray(other, dtype=np.float32))[None].to(hd.device)
+        _, d, _ = reward_signal_device(hd, None, cd, self.cfg, estimator="delta", other=od)
+        return d[0].double().cpu().numpy()
 
 
 def reward(h, c, cfg=None, region="full"):
@@ -116,12 +146,11 @@ def reward(h, c, cfg=None, region="full"):
 
 
 def delta_map(ctx, other_values):
-    """metrics.py:333-358 for binary edits: R(pixel a -> other[a]) - R(h)."""
+    """metrics.py:333-358: R(pixel a -> other[a]) - R(h) for every pixel a
+    (0 where other == h)."""
     other = np.asarray(other_values, dtype=np.float64)
     if other.shape != ctx.h.shape:
         raise ValueError("other_values shape mismatch")
-    if not np.all((other == 0.0) | (other == 1.0)):
-        raise NotImplementedError("non-binary substitutions (multitone) are outside the GPU path")
     hgt, wid = ctx.h.shape
     ctx.eval_count += hgt * wid
-    return np.where(other != ctx.h, ctx._flip_delta, 0.0)
+    return ctx.delta(other)

@@ -230,7 +230,7 @@ class PolicyNetwork:
                   _lib.ptr(grad), _lib.ptr(dx), _lib.stream_ptr())
 
     def halftone_device(self, c, z, p_out=None, h_out=None, pbm_out=None, impl=None,
-                        rows=None, workspace=None, check=False, stream=None):
+                        rows=None, workspace=None, check=False, stream=None, levels=2):
         """Fused inference forward + threshold (K1) on device tensors.
 
         c, z: (B, in_rows, W) float32 contone / noise (rows [in_row0,
@@ -238,7 +238,8 @@ class PolicyNetwork:
         out_rows), default the whole image).  Outputs (B, out_rows, W):
         p_out float32, h_out uint8 (1 = white), pbm_out PBM P4 payload
         (B, out_rows, ceil(W/8)).  impl 0 = tcgen05 fused kernel (default for
-        the paper architecture), 1 = fp32 SIMT cross-check path."""
+        the paper architecture), 1 = fp32 SIMT cross-check path.  levels > 2:
+        h_out receives the multitone level index (multitone.py:61-76)."""
         torch = _torch()
         self.sync()
         if c.dim() == 2:
@@ -256,10 +257,18 @@ class PolicyNetwork:
         if workspace is None or workspace.numel() < nbytes:
             workspace = torch.empty(nbytes, dtype=torch.uint8, device=c.device)
         sp = _lib.stream_ptr(stream)
-        _lib.call("ht_halftone", _lib.ptr(self._packed), self.channels, self.blocks,
-                  _lib.ptr(c.contiguous()), _lib.ptr(z.contiguous()), B, H, W, in_row0, in_rows,
-                  out_row0, out_rows, _lib.ptr(p_out), _lib.ptr(h_out), _lib.ptr(pbm_out),
-                  _lib.ptr(workspace), nbytes, impl, sp)
+        if levels == 2:
+            _lib.call("ht_halftone", _lib.ptr(self._packed), self.channels, self.blocks,
+                      _lib.ptr(c.contiguous()), _lib.ptr(z.contiguous()), B, H, W, in_row0,
+                      in_rows, out_row0, out_rows, _lib.ptr(p_out), _lib.ptr(h_out),
+                      _lib.ptr(pbm_out), _lib.ptr(workspace), nbytes, impl, sp)
+        else:
+            if pbm_out is not None:
+                raise ValueError("the PBM payload is binary (levels = 2)")
+            _lib.call("ht_multitone", _lib.ptr(self._packed), self.channels, self.blocks,
+                      _lib.ptr(c.contiguous()), _lib.ptr(z.contiguous()), B, H, W, in_row0,
+                      in_rows, out_row0, out_rows, int(levels), _lib.ptr(p_out), _lib.ptr(h_out),
+                      _lib.ptr(workspace), nbytes, impl, sp)
         if check:
             _lib.call("ht_halftone_check", _lib.ptr(workspace), sp)
         return workspace

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .hvs import HvsConfig
 from .imagecore import Rng, gaussian_noise_map, gaussian_noise_map_device, random_crop
-from .metrics import MetricConfig, reward, reward_le_device
+from .metrics import MetricConfig, reinforce_signal_device, reward, reward_signal_device
 from .nn import Adam, PolicyNetwork, cosine_lr, load_checkpoint
 from .spectral import anisotropy_device, ring_partition
 
@@ -74,37 +74,112 @@ def infer_halftone(net, c, rng, impl=None):
 
 
 # ---------------------------------------------------------------------------
-# sampling / estimators (binary policy)
+# sampling / estimators (host API of the reference; rewards on the GPU)
+
+PROB_FLOOR = 1e-7   # rl.py:34, clamp before the log-derivative division
+
+
+def _cast_two_point(values, level_count):
+    """rl.py:40-57: the two lattice levels around each value (levels
+    i/(L-1)) and the upper-level mass; on-lattice values collapse."""
+    v = np.asarray(values, dtype=np.float64)
+    if np.any(v < 0.0) or np.any(v > 1.0):
+        raise ValueError("values outside [0, 1]")
+    steps = level_count - 1
+    scaled = v * steps
+    idx = np.floor(scaled)
+    frac = scaled - idx
+    floor_vals = idx / steps
+    ceil_vals = np.where(frac == 0.0, floor_vals, np.minimum(idx + 1.0, steps) / steps)
+    return floor_vals, ceil_vals, frac
+
+
+def sample_actions(p, rng):
+    """rl.py:60-64: independent Bernoulli(p), one uniform per pixel, row-major."""
+    p = np.asarray(p, dtype=np.float64)
+    return (rng.uniforms(p.size).reshape(p.shape) < p).astype(np.float64)
+
+
+def _sample_two_point(floor_vals, ceil_vals, p_ceil, rng):
+    """rl.py:67-69."""
+    u = rng.uniforms(p_ceil.size).reshape(p_ceil.shape)
+    return np.where(u < p_ceil, ceil_vals, floor_vals)
+
 
 @dataclass
 class EpisodeSample:
-    """rl.py:72-82 (binary: floor 0, ceil 1, p_ceil = p)."""
+    """rl.py:72-82."""
     c: np.ndarray
     z: np.ndarray
     p: np.ndarray
     m: np.ndarray
+    floor_vals: np.ndarray
+    ceil_vals: np.ndarray
+    p_ceil: np.ndarray
     level_count: int
     ctx: object
 
 
 def make_sample(p, c, z, rng, cfg=None, level_count=2):
-    """rl.py:85-93 for L=2: m = (u < p) with row-major uniforms, reward
-    context built on the GPU."""
-    if level_count != 2:
-        raise NotImplementedError("multitone (L>2) is outside the GPU hot path")
-    p = np.asarray(p, dtype=np.float64)
-    u = rng.uniforms(p.size).reshape(p.shape)
-    m = (u < p).astype(np.float64)
+    """rl.py:85-93: sample the cast policy, reward context built on the GPU."""
+    floor_vals, ceil_vals, p_ceil = _cast_two_point(p, level_count)
+    m = _sample_two_point(floor_vals, ceil_vals, p_ceil, rng)
     ctx = reward(m, c, cfg or MetricConfig(), region="full")
-    return EpisodeSample(c=c, z=z, p=p, m=m, level_count=2, ctx=ctx)
+    return EpisodeSample(c=c, z=z, p=np.asarray(p, dtype=np.float64), m=m, floor_vals=floor_vals,
+                         ceil_vals=ceil_vals, p_ceil=p_ceil, level_count=level_count, ctx=ctx)
+
+
+def _two_point_diff(sample):
+    """rl.py:96-103: R(upper) - R(lower) per pixel (0 where collapsed)."""
+    from .metrics import delta_map
+    at_ceil = sample.m == sample.ceil_vals
+    other = np.where(at_ceil, sample.floor_vals, sample.ceil_vals)
+    return np.where(at_ceil, -1.0, 1.0) * delta_map(sample.ctx, other)
 
 
 def le_signal(sample):
-    """rl.py:106-109: dL/dp_a = -(R(up) - R(down)) / delta, delta = 1."""
+    """rl.py:106-109: dL/dp_a = -(R(up) - R(down)) / delta."""
+    return -_two_point_diff(sample) * (sample.level_count - 1)
+
+
+def _dlogpi(p, h):
+    p = np.clip(p, PROB_FLOOR, 1.0 - PROB_FLOOR)
+    return np.where(h == 1.0, 1.0 / p, -1.0 / (1.0 - p))
+
+
+def coma_signal(sample):
+    """rl.py:117-129: counterfactual-baseline gradient (binary only)."""
     from .metrics import delta_map
-    d_other = delta_map(sample.ctx, 1.0 - sample.m)
-    sign = np.where(sample.m == 1.0, -1.0, 1.0)
-    return -(sign * d_other)
+    if sample.level_count != 2:
+        raise ValueError("coma_signal requires a binary policy")
+    h = sample.m
+    r_cur = sample.ctx.reward
+    r_flip = r_cur + delta_map(sample.ctx, 1.0 - h)
+    r_up = np.where(h == 1.0, r_cur, r_flip)
+    r_down = np.where(h == 0.0, r_cur, r_flip)
+    p = np.clip(sample.p, PROB_FLOOR, 1.0 - PROB_FLOOR)
+    return -_dlogpi(sample.p, h) * (r_cur - (p * r_up + (1.0 - p) * r_down))
+
+
+def reinforce_signal(sample, baseline=0.0):
+    """rl.py:132-136: score-function gradient, optional scalar baseline."""
+    if sample.level_count != 2:
+        raise ValueError("reinforce_signal requires a binary policy")
+    return -_dlogpi(sample.p, sample.m) * (sample.ctx.reward - baseline)
+
+
+def _signals_for_batch(samples, estimator):
+    """rl.py:219-229 (host API; train_step runs the device kernels)."""
+    if estimator == "local_expectation":
+        return [le_signal(s) for s in samples]
+    if estimator == "coma":
+        return [coma_signal(s) for s in samples]
+    if estimator == "reinforce":
+        return [reinforce_signal(s) for s in samples]
+    if estimator == "reinforce_meanbaseline":
+        mean_r = float(np.mean([s.ctx.reward for s in samples]))
+        return [reinforce_signal(s, baseline=mean_r) for s in samples]
+    raise ValueError(f"unknown estimator {estimator!r}")
 
 
 # ---------------------------------------------------------------------------
@@ -154,9 +229,6 @@ class TrainConfig:
             raise ValueError("channels must be positive and blocks non-negative")
         if self.log_every < 1 or self.checkpoint_every < 0:
             raise ValueError("log_every must be positive and checkpoint_every non-negative")
-        if self.estimator != "local_expectation" or self.levels != 2:
-            raise NotImplementedError("the GPU training path implements the binary "
-                                      "local_expectation estimator (rl.py:106-109)")
 
 
 from .parallel import allreduce_sum_, shard_range  # noqa: E402
@@ -213,9 +285,25 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
             us.append(rng.uniforms_device(size * size, device=dev).view(size, size))
         else:
             rng.jump(size * size)
+    reinforce = cfg.estimator in ("reinforce", "reinforce_meanbaseline")
     if hi > lo:
         ud = torch.stack(us)
-        m, sig, rew = reward_le_device(p, ud, cd, mcfg, scale=1.0 / bs)
+        if not reinforce:
+            m, sig, rew = reward_signal_device(p, ud, cd, mcfg, scale=1.0 / bs, levels=cfg.levels,
+                                               estimator=cfg.estimator)
+        else:
+            m, _, rew = reward_signal_device(p, ud, cd, mcfg, want_signal=False)
+    if cfg.estimator == "reinforce_meanbaseline":
+        # baseline = mean reward of the GLOBAL batch: one extra scalar
+        # all-reduce, joined by every rank (also those without samples)
+        rsum = rew.sum().reshape(1) if hi > lo else torch.zeros(1, dtype=torch.float64, device=dev)
+        allreduce_sum_(rsum, group=group)
+        baseline = float(rsum.item()) / bs
+    else:
+        baseline = 0.0
+    if hi > lo:
+        if reinforce:
+            sig = reinforce_signal_device(p, m, rew, baseline, scale=1.0 / bs)
         if signal_override is not None:
             mh = m.double().cpu().numpy()
             sig = torch.from_numpy(np.stack([signal_override(lo + i, mh[i]) / bs

@@ -74,7 +74,8 @@ def test_reward_delta_le(model):
     assert abs(ctx.reward / g[f"{model}_reward"][0] - 1) < 1e-10
     d = metrics.delta_map(ctx, 1.0 - g["m"])
     assert rel(d, g[f"{model}_delta_flip"]) < 1e-6       # fp32 signal storage
-    s = rl.EpisodeSample(c=g["c"], z=None, p=None, m=g["m"], level_count=2, ctx=ctx)
+    s = rl.EpisodeSample(c=g["c"], z=None, p=None, m=g["m"], floor_vals=np.zeros_like(g["m"]),
+                         ceil_vals=np.ones_like(g["m"]), p_ceil=None, level_count=2, ctx=ctx)
     assert rel(rl.le_signal(s), g[f"{model}_le"]) < 1e-6
 
 
