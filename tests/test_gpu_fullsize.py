@@ -1,0 +1,151 @@
+"""BASELINE configs 2-5 at their full sizes, through size-independent
+properties (the oracle cannot run whole 512^2 images or the 35-Mpixel page in
+test time):
+
+* window rule: the fused kernel's output on a 64x64 window of a full image
+  equals the oracle run on that window's input with a 34-pixel halo (the
+  receptive field of the 34 stacked 3x3 convs), by the 1e-3 / band rule;
+* config 3: RAPSD + anisotropy of the GPU halftones of all 256 gray levels
+  equal the oracle's spectra of the same halftones (1e-4 relative);
+* config 4: the 7016x4960 page halftoned unsharded and in 2/4/8 row strips
+  (34-row halos) stitches bitwise;
+* config 5: the data-parallel decomposition (two shards with the global
+  1/batch scaling, summed) equals the single-process gradient.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import htoracle as O
+from paper_2304_12152_b200 import synth
+from paper_2304_12152_b200.imagecore import Rng
+
+pytestmark = pytest.mark.gpu
+HALO = 34
+P_TOL = 1e-3
+
+
+def _net(std=0.05):
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(32, 16)
+    net.init_params(Rng(0), std=std)
+    return net
+
+
+def _check_window(net, c, z, p_full, h_full, y0, x0, size=64):
+    """Oracle on the haloed window vs the full-image kernel output."""
+    H, W = c.shape
+    a0, a1 = max(0, y0 - HALO), min(H, y0 + size + HALO)
+    b0, b1 = max(0, x0 - HALO), min(W, x0 + size + HALO)
+    params = [p.value for p in net.params()]
+    x = np.stack((c[a0:a1, b0:b1], z[a0:a1, b0:b1])).astype(np.float64)[None]
+    p_ref = O.policy_forward(params, x)[0, 0][y0 - a0:y0 - a0 + size, x0 - b0:x0 - b0 + size]
+    p = p_full[y0:y0 + size, x0:x0 + size]
+    h = h_full[y0:y0 + size, x0:x0 + size]
+    assert np.max(np.abs(p - p_ref)) <= P_TOL
+    band = np.abs(p_ref - 0.5) < 1e-3
+    assert np.array_equal(h[~band], (p_ref >= 0.5)[~band].astype(h.dtype))
+
+
+def test_config2_full_batch_windows():
+    """64 x 512^2 (10% with step edges) in one call; windows of two images
+    (one with a step edge, one image-border window) against the oracle."""
+    from paper_2304_12152_b200 import rl
+    net = _net()
+    c = synth.config_batch(64, 512, 512, seed=2, blobs=8, rects=2, step_frac=0.1).astype(np.float32)
+    z = np.stack([Rng(100 + i).gaussians_f32(512 * 512).reshape(512, 512) for i in range(64)])
+    h, p = rl.halftone(net, c, z)
+    assert h.shape == (64, 512, 512)
+    for i, y0, x0 in ((0, 224, 200), (37, 0, 448)):
+        _check_window(net, c[i], z[i], p[i], h[i], y0, x0)
+    # batch invariance at full size: image 37 alone is bitwise the same
+    h1, p1 = rl.halftone(net, c[37], z[37])
+    assert np.array_equal(p1, p[37]) and np.array_equal(h1, h[37])
+
+
+def test_config3_gray_sweep_spectra():
+    """256 flat grays g = k/255 at 256^2: halftones (window rule on three
+    levels) and the per-level RAPSD / anisotropy of those same halftones."""
+    import torch
+    from paper_2304_12152_b200 import rl, spectral
+    net = _net()
+    n = 256
+    c = np.stack([np.full((n, n), k / 255.0, dtype=np.float32) for k in range(256)])
+    z = np.stack([Rng(500 + k).gaussians_f32(n * n).reshape(n, n) for k in range(256)])
+    h, p = rl.halftone(net, c, z)
+    for k in (0, 128, 255):
+        _check_window(net, c[k], z[k], p[k], h[k], 96, 96)
+    part = spectral.ring_partition((n, n))
+    power, anis, dc = spectral.rapsd_device(torch.from_numpy(h.astype(np.float32)).cuda(), part)
+    power, anis, dc = power.cpu().numpy(), anis.cpu().numpy(), dc.cpu().numpy()
+    assert power.shape == (256, 181)
+    opart = O.ring_partition((n, n))
+    for k in (1, 64, 127, 128, 200, 254):
+        pw, an, d0 = O.rapsd(O.periodogram(h[k]), opart)
+        assert np.allclose(power[k], pw, rtol=1e-4, atol=1e-12)
+        ok = np.isfinite(an)
+        assert np.array_equal(ok, np.isfinite(anis[k]))
+        assert np.allclose(anis[k][ok], an[ok], rtol=1e-4)
+        assert abs(dc[k] - d0) <= 1e-9 * max(1.0, abs(d0))
+
+
+def test_config4_page_row_strips_bitwise():
+    """7016 x 4960 page: unsharded vs 2/4/8 row strips with 34-row halos,
+    stitched bitwise; two windows (page interior, strip seam) vs the oracle."""
+    import torch
+    from paper_2304_12152_b200.imagecore import gaussian_noise_map_device
+    from paper_2304_12152_b200.parallel import row_strip
+    net = _net()
+    H, W = 7016, 4960
+    page = synth.contone(H, W, seed=4, blobs=64, rects=16).astype(np.float32)
+    zd = gaussian_noise_map_device(Rng(4), W, H)
+    cd = torch.from_numpy(page).cuda()
+    h_full = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
+    p_full = torch.empty((1, H, W), dtype=torch.float32, device="cuda")
+    ws = net.halftone_device(cd[None], zd[None], p_out=p_full, h_out=h_full, check=True)
+    del ws
+    for world in (2, 4, 8):
+        out = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+        for rank in range(world):
+            s = row_strip(H, rank, world)
+            hs = torch.empty((1, s.out_rows, W), dtype=torch.uint8, device="cuda")
+            net.halftone_device(cd[s.in_row0:s.in_row0 + s.in_rows][None],
+                                zd[s.in_row0:s.in_row0 + s.in_rows][None], h_out=hs,
+                                rows=s.as_kernel_rows(H), check=True)
+            out[s.out_row0:s.out_row0 + s.out_rows] = hs[0]
+        assert torch.equal(out, h_full[0]), f"world={world}"
+    z = zd.cpu().numpy()
+    pf, hf = p_full[0].cpu().numpy(), h_full[0].cpu().numpy()
+    seam = row_strip(H, 1, 8).out_row0
+    for y0, x0 in ((3500, 2400), (seam - 32, 4960 - 64)):
+        _check_window(net, page, z, pf, hf, y0, x0)
+
+
+def test_config5_data_parallel_gradient_full_size(monkeypatch):
+    """16 x 256^2 + 4 gray, LE + anisotropy: two data-parallel shards (run one
+    after the other on this GPU, all-reduce replaced by a host sum) give the
+    single-process gradient."""
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    cfg = rl.TrainConfig(iterations=10, batch_size=16, crop_size=256, anisotropy_batch_size=4,
+                         hvs_model="gaussian")
+    ds = [synth.contone(512, 512, seed=s).astype(np.float64) for s in range(3)]
+
+    def grad_of(rank, world):
+        net = PolicyNetwork(32, 16)
+        rng = Rng(0)
+        net.init_params(rng)
+        captured = {}
+        monkeypatch.setattr(rl, "_dist_info", lambda group=None: (rank, world))
+        monkeypatch.setattr(rl, "allreduce_sum_", lambda *t, group=None: captured.setdefault("t", t))
+        rl.train_step(net, Adam(net.params()), ds, cfg, rng, 0)
+        g, stats = captured["t"]
+        return g.double().cpu().numpy(), stats.cpu().numpy(), rng.state_words()
+
+    g1, s1, st1 = grad_of(0, 1)
+    ga, sa, sta = grad_of(0, 2)
+    gb, sb, stb = grad_of(1, 2)
+    assert st1 == sta == stb                     # every rank consumed the same stream
+    rel = np.linalg.norm(ga + gb - g1) / np.linalg.norm(g1)
+    assert rel < 1e-6
+    assert np.allclose(sa + sb, s1, rtol=1e-6)
