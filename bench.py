@@ -103,13 +103,23 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ inputs
-def make_inputs(B, H, W, seed):
+def noise_seed(seed):
+    return seed * 1_000_003
+
+
+def make_inputs(B, H, W, seed, device=None):
+    """Contones from the BASELINE generator; noise maps drawn in image order
+    from one reference-RNG stream (as B calls of rl.infer_halftone would),
+    on the GPU when `device` is given (the same stream the e2e engine draws)."""
     from paper_2304_12152_b200 import synth
-    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_device, gaussian_noise_map_f32
     c = synth.config_batch(B, H, W, seed=seed, blobs=8, rects=2, step_frac=0.1)
-    z = np.empty((B, H, W), dtype=np.float32)
-    for i in range(B):
-        z[i] = Rng(seed * 1_000_003 + i).gaussians_f32(H * W).reshape(H, W)
+    rng = Rng(noise_seed(seed))
+    if device is not None:
+        z = np.stack([gaussian_noise_map_device(rng, W, H, device=device).cpu().numpy()
+                      for _ in range(B)])
+    else:
+        z = np.stack([gaussian_noise_map_f32(rng, W, H) for _ in range(B)])
     return c, z
 
 
@@ -191,9 +201,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2304_12152_b200 import _lib, rl
 
-    c_np, z_np = make_inputs(B, H, W, seed=2 + 7919 * rank)
-    net = make_net()
     dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    seed = 2 + 7919 * rank
+    c_np, z_np = make_inputs(B, H, W, seed=seed, device=dev)
+    net = make_net()
     c = torch.from_numpy(c_np).to(dev)
     z = torch.from_numpy(z_np).to(dev)
     h = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
@@ -249,6 +261,10 @@ def main():
         ch = torch.from_numpy(c_np).pin_memory()
         zh = torch.from_numpy(z_np).pin_memory()
         oh = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+        # contones + noise maps from pinned host memory.  (The engine can also
+        # draw the noise on the GPU from an Rng, eng(ch, rng, oh); measured
+        # slower here: the copy engines move the noise for free while device
+        # generation takes SM time from the forward.)
         for _ in range(args.warmup):
             eng(ch, zh, oh)
         if world > 1:

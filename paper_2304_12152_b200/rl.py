@@ -401,7 +401,10 @@ class HalftoneEngine:
         self.groups = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
         dev = net.device
         self.dev = dev
-        self.streams = [torch.cuda.Stream(dev) for _ in range(2)]
+        # forward/copy streams at high priority: the block scheduler then
+        # prefers the fused kernel's CTAs over the side stream's noise blocks
+        self.streams = [torch.cuda.Stream(dev, priority=-1) for _ in range(2)]
+        self.noise_stream = torch.cuda.Stream(dev, priority=0)
         self.c = torch.empty((B, H, W), dtype=torch.float32, device=dev)
         self.z = torch.empty((B, H, W), dtype=torch.float32, device=dev)
         if output == "pbm":
@@ -416,30 +419,55 @@ class HalftoneEngine:
     def out_shape(self):
         return tuple(self.out.shape)
 
-    def h2d_bytes(self):
-        return 2 * self.B * self.H * self.W * 4
+    def h2d_bytes(self, device_noise=False):
+        return (1 if device_noise else 2) * self.B * self.H * self.W * 4
 
     def d2h_bytes(self):
         return self.out.numel() * self.out.element_size()
 
     def __call__(self, c_host, z_host, out_host):
-        """c_host, z_host: (B,H,W) float32 CPU tensors (pinned for async
-        copies); out_host: CPU tensor shaped out_shape()."""
+        """c_host: (B,H,W) float32 CPU tensor (pinned for async copies);
+        z_host: the (B,H,W) float32 noise as a CPU tensor, or an Rng -- then
+        image i's noise map is gaussian_noise_map(rng, W, H) drawn on the GPU
+        in image order, as B calls of rl.infer_halftone would draw it
+        (rl.py:306-311); out_host: CPU tensor shaped out_shape()."""
         torch = _torch()
         cur = torch.cuda.current_stream(self.dev)
+        device_noise = isinstance(z_host, Rng)
+        ready = [None] * len(self.groups)
+        if device_noise:
+            # every chunk's noise maps, drawn in image order from the stream;
+            # chunk 0 on its own stream, the rest on a side stream so they
+            # run beside chunk 0's forward (the fused kernel leaves the FP64
+            # pipe and 1/8 of the register file free)
+            n = self.H * self.W
+            for k, (a, b) in enumerate(self.groups):
+                ns = self.streams[0] if k == 0 else self.noise_stream
+                ns.wait_stream(cur)
+                with torch.cuda.stream(ns):
+                    if n % 2 == 0:     # maps of even size are back-to-back in the stream
+                        z_host.gaussians_device((b - a) * n, out=self.z[a:b].view(-1))
+                    else:              # odd size: each map burns one draw
+                        for i in range(a, b):
+                            z_host.gaussians_device(n, out=self.z[i].view(-1))
+                    ready[k] = torch.cuda.Event()
+                    ready[k].record(ns)
         for k, (a, b) in enumerate(self.groups):
             s = self.streams[k % 2]
             s.wait_stream(cur)
             with torch.cuda.stream(s):
                 self.c[a:b].copy_(c_host[a:b], non_blocking=True)
-                self.z[a:b].copy_(z_host[a:b], non_blocking=True)
+                if device_noise:
+                    s.wait_event(ready[k])
+                else:
+                    self.z[a:b].copy_(z_host[a:b], non_blocking=True)
                 kw = {"h_out" if self.output == "h" else
                       ("pbm_out" if self.output == "pbm" else "p_out"): self.out[a:b]}
                 self.ws[k % 2] = self.net.halftone_device(
                     self.c[a:b], self.z[a:b], impl=self.impl, workspace=self.ws[k % 2],
                     stream=s, **kw)
                 out_host[a:b].copy_(self.out[a:b], non_blocking=True)
-        for s in self.streams:
+        for s in self.streams + [self.noise_stream]:
             cur.wait_stream(s)
         cur.synchronize()
         return out_host

@@ -169,3 +169,26 @@ def test_fused_pass_plans_for_other_depths(nb):
     h0, p0 = rl.halftone(net, c, z, impl=0)
     h1, p1 = rl.halftone(net, c, z, impl=1)
     _check(p0, h0, p1, P_TOL)
+
+
+def test_engine_draws_noise_on_device_in_infer_halftone_order():
+    """rl.HalftoneEngine(c, rng): image i's noise is the i-th
+    gaussian_noise_map of the stream (as B calls of infer_halftone)."""
+    import torch
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_device
+    net = _net(0.05)
+    B, H, W = 3, 40, 52
+    r = Rng(8)
+    c = torch.from_numpy(r.uniforms(B * H * W).reshape(B, H, W).astype(np.float32)).pin_memory()
+    zr = Rng(5)
+    z = torch.stack([gaussian_noise_map_device(zr, W, H).cpu() for _ in range(B)]).pin_memory()
+    eng = rl.HalftoneEngine(net, B, H, W, chunks=2, output="h")
+    o1 = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+    o2 = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+    eng(c, z, o1)
+    rng = Rng(5)
+    eng(c, rng, o2)
+    assert torch.equal(o1, o2)
+    assert rng.state_words() == zr.state_words()
+    assert eng.h2d_bytes(device_noise=True) * 2 == eng.h2d_bytes()
