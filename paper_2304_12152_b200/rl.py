@@ -397,7 +397,11 @@ class HalftoneEngine:
         self.output = output
         self.impl = impl
         chunks = max(1, min(chunks, B))
-        bounds = np.linspace(0, B, chunks + 1).round().astype(int)
+        # a small first chunk (its H2D is the one copy nothing overlaps), the
+        # rest split evenly so the fused kernel keeps long strips per CTA
+        first = max(1, -(-B // 16)) if chunks > 1 else B
+        rest = np.linspace(first, B, chunks).round().astype(int)
+        bounds = [0] + [int(x) for x in rest]
         self.groups = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
         dev = net.device
         self.dev = dev
