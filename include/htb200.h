@@ -127,12 +127,26 @@ int ht_last_launch_count(int *count);
 int ht_timing_enable(int on);
 int ht_timing_read(int *tags, float *ms, int max, int *count);
 
+/* Training convolutions (nn.py:46-77): 0 = the 32 -> 32 convs of the residual
+ * blocks (forward and input-gradient) on tcgen05 with 3xTF32 operands
+ * (default), 1 = fp32 SIMT kernels only (cross-check).  Process-wide. */
+int ht_set_train_conv_impl(int impl);
+/* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
+ * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +
+ * bias, zeroed where mask <= 0, + resid, ReLU if relu -- Conv2d.forward
+ * (nn.py:46-60) and the epilogues of the block backward (nn.py:97-100) --
+ * on impl 0 (tcgen05) or 1 (fp32 SIMT).  For parity tests. */
+int ht_conv3x3_32(const float *x, int B, int H, int W, const float *w, const float *bias,
+                  const float *mask, const float *resid, float *out, int relu, int impl,
+                  void *stream);
+
 /* ---- K1' / K2: training forward (stores activations) and backward -------
  * Replaces PolicyNetwork.forward/backward (nn.py:138-160) incl.
  * ResidualBlock (nn.py:91-100) and Conv2d (nn.py:46-77), fp32 math.
  * x_dev: (B, 2, H, W) float32.  act_dev: ht_train_act_bytes() bytes.
  * p_dev: (B, H, W) float32 output.  Returns HT_E_NONFINITE on non-finite
- * logits (nn.py:147-148). */
+ * logits (nn.py:147-148).  The 32 -> 32 convs run on tcgen05 (3xTF32), the
+ * rest in fp32 SIMT (see ht_set_train_conv_impl). */
 int ht_train_act_bytes(int channels, int blocks, int B, int H, int W,
                        int64_t *bytes);
 int ht_policy_forward_train(const void *packed_dev, int channels, int blocks,

@@ -61,6 +61,8 @@ void timing_mark_end(cudaStream_t st) {
   cudaEventRecord(g_timed.back().b, st);
 }
 
+int g_train_conv_impl = 0;
+
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
 static inline uint64_t splitmix64(uint64_t &s) {
   s += 0x9E3779B97F4A7C15ull;
@@ -118,6 +120,14 @@ int ht_timing_read(int *tags, float *ms, int max, int *count) {
   }
   ht::g_timed.clear();
   *count = n;
+  return HT_OK;
+}
+
+// Training convolutions: 0 = tcgen05 3xTF32 kernel for the 32 -> 32 convs
+// (default), 1 = fp32 SIMT kernels only (cross-check).
+int ht_set_train_conv_impl(int impl) {
+  if (impl != 0 && impl != 1) return ht::fail(HT_E_INVALID, "impl must be 0 (tensor core) or 1 (simt)");
+  ht::g_train_conv_impl = impl;
   return HT_OK;
 }
 

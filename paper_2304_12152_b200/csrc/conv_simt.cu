@@ -214,10 +214,18 @@ __global__ void threshold_window_kernel(const float *__restrict__ logit, int B, 
 // host orchestration
 namespace ht {
 
+// conv_tc.cu: the 32 -> 32 training conv on tcgen05 (3xTF32)
+int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+              const float *resid, float *out, int relu, cudaStream_t st);
+extern int g_train_conv_impl;   // 0: tensor cores for 32 -> 32 convs (default), 1: SIMT only
+
 template <int CIN, int COUT>
 static int conv_fwd(const float *x, int B, int H, int W, const float *w, const float *bias,
                     const float *mask, const float *resid, float *out, int relu,
                     cudaStream_t st) {
+  if constexpr (CIN == 32 && COUT == 32) {
+    if (g_train_conv_impl == 0) return conv_tc32(x, B, H, W, w, bias, mask, resid, out, relu, st);
+  }
   dim3 grid((W + FT_X - 1) / FT_X, (H + FT_Y - 1) / FT_Y, B);
   conv3x3_fwd_kernel<CIN, COUT><<<grid, 128, 0, st>>>(x, H, W, w, bias, mask, resid, out, relu);
   count_launch();
@@ -417,6 +425,21 @@ int ht_policy_backward(const void *packed, int C, int NB, const float *x, int B,
     }
   });
   return HT_OK;
+}
+
+
+// One 3x3 convolution 32 -> 32 (x, out, mask, resid: (B, 32, H, W) fp32; w
+// OIHW fp32), the training conv with its epilogue options, on the chosen
+// implementation: 0 = tcgen05 split-bf16, 1 = fp32 SIMT.  For tests.
+int ht_conv3x3_32(const float *x, int B, int H, int W, const float *w, const float *bias,
+                  const float *mask, const float *resid, float *out, int relu, int impl, void *stream) {
+  HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty input");
+  HT_REQUIRE(impl == 0 || impl == 1, "impl must be 0 (tensor core) or 1 (simt)");
+  const int keep = ht::g_train_conv_impl;
+  ht::g_train_conv_impl = impl;
+  const int rc = ht::conv_fwd<32, 32>(x, B, H, W, w, bias, mask, resid, out, relu, (cudaStream_t)stream);
+  ht::g_train_conv_impl = keep;
+  return rc;
 }
 
 }  // extern "C"

@@ -1,0 +1,355 @@
+// Training 3x3 convolution 32 -> 32 on tcgen05 with split-bf16 operands.
+//
+// Replaces conv3x3_fwd_kernel<32,32> of the training path: the residual
+// blocks' forward convs (nn.py:46-60, 91-95) and their input gradients, which
+// conv_simt.cu runs as forward convs with transposed / flipped weights
+// (nn.py:62-77, 97-100).  Same epilogue options: bias, ReLU mask, residual
+// add, ReLU.  NCHW fp32 in and out, so the rest of the pipeline is unchanged.
+//
+// Precision: each fp32 operand is split into three bf16 parts x = x0 + x1 +
+// x2 (x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1): 24 mantissa
+// bits, the fp32 exponent range); a product keeps the six terms xi*wj with
+// i + j <= 2, accumulated in fp32 TMEM (six kind::f16 MMAs, bf16 rate =
+// 2x tf32), i.e. fp32-level accuracy -- needed: with 3xTF32 (~2^-21 per
+// product) the 32 chained input-gradient convs of the paper architecture
+// missed the 1e-4 bar (1.3e-3).
+//
+// Structure (the fused forward's row streaming, one layer):
+// * a strip is 128 pixel lanes of the virtual side-by-side image (the B
+//   images laid next to each other with one zero column between), with 126
+//   output lanes (halo 1);
+// * rows stream top to bottom; MMA(r) for input row r adds into output rows
+//   r+1, r, r-1, a 3-slot TMEM ring reached through a window of the doubled
+//   ky sequence [2,1,0,2,1] (N = 96), 36 MMAs per row (3 kx x 2 K-halves x
+//   6 split products);
+// * one CTA per SM: the weights (three bf16 parts, 90 KB) are split into
+//   UMMA tiles by every CTA from the OIHW fp32 tensor, two input rows (three
+//   parts, 48 KB) are double buffered; 4 warps, thread = pixel lane.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+#include <cuda_bf16.h>
+
+namespace ht {
+namespace tct {
+
+using namespace ::ht::tc;
+
+constexpr int C = 32;
+constexpr int M = 128;
+constexpr int S = M - 2;              // output lanes per strip
+constexpr int NSL = 5;                // doubled ky sequence [2,1,0,2,1]
+constexpr int NPART = 3;              // bf16 parts of an fp32 value
+constexpr int PLANE = M * 16;         // 8 channels x 128 lanes (bf16)
+constexpr int ROW = 4 * PLANE;        // 32 channels of a row, one part
+constexpr int TILE = 2 * NSL * C * 16;  // B tile for (kx, 16-channel K-half): 160 rows x 32 B
+constexpr int W_BYTES = NPART * 3 * 2 * TILE;
+constexpr int A_OFF = W_BYTES;
+constexpr int A_BYTES = 2 * NPART * ROW;    // 2 buffers x 3 parts
+constexpr int BAR_OFF = A_OFF + A_BYTES;
+constexpr int SMEM = BAR_OFF + 16 + 16;
+constexpr int CORR_COL = 3 * 3 * C;   // TMEM column of the correction ring
+constexpr uint32_t IDESC_BF16 =
+    (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+__constant__ int c_ky[NSL] = {2, 1, 0, 2, 1};
+
+// x = x0 + x1 + x2 (bf16 parts; the remainders are exact in fp32)
+__device__ __forceinline__ void split3(float x, __nv_bfloat16 &p0, __nv_bfloat16 &p1, __nv_bfloat16 &p2) {
+  p0 = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(p0);
+  p1 = __float2bfloat16_rn(r1);
+  p2 = __float2bfloat16_rn(r1 - __bfloat162float(p1));
+}
+__device__ __forceinline__ uint32_t pack_bf2(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+
+// One input row: for kx in 0..2, K-half kh in 0..1 (16 channels) and the six
+// split products (i, j) with i + j <= 2: D[128 x 96] += A_i[128 x 16] * B_j[96 x 16]^T.
+// The main products (0, 0) go to this input row's own ring d_main (the first
+// overwrites it: no re-init), the five smaller correction products to the
+// shared ring d_corr -- short accumulation chains for the large terms keep
+// the tensor core's fp32 accumulation error at the SIMT level.
+// Descriptors are the six bases plus immediate offsets (16-B units).
+__device__ __forceinline__ void mma36_row(uint32_t d_main, uint32_t d_corr, uint64_t a0, uint64_t a1,
+                                          uint64_t a2, uint64_t b0, uint64_t b1, uint64_t b2,
+                                          uint32_t bar_acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, z;\n\t.reg .b64 ta, tb;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "setp.ne.b32 z, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, z;\n\t"
+      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, -1;\n\tadd.s64 tb, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %7, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, -1;\n\tadd.s64 tb, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, -1;\n\tadd.s64 tb, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %5, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %6, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 255;\n\tadd.s64 tb, %5, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %7, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 255;\n\tadd.s64 tb, %6, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, 255;\n\tadd.s64 tb, %5, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %5, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %6, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 0;\n\tadd.s64 tb, %5, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %7, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 0;\n\tadd.s64 tb, %6, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, 0;\n\tadd.s64 tb, %5, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %5, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %6, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 256;\n\tadd.s64 tb, %5, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %7, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 256;\n\tadd.s64 tb, %6, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, 256;\n\tadd.s64 tb, %5, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %6, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %7, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 1;\n\tadd.s64 tb, %6, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %6, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %7, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %3, 257;\n\tadd.s64 tb, %6, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "add.s64 ta, %4, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}"
+      ::"r"(d_main), "r"(d_corr), "l"(a0), "l"(a1), "l"(a2), "l"(b0), "l"(b1), "l"(b2), "r"(IDESC_BF16),
+        "r"(bar_acc)
+      : "memory");
+}
+
+struct ConvParams {
+  const float *x, *w, *bias, *mask, *resid;
+  float *out;
+  int B, H, W, VW, relu;
+  int n_strips;
+  long long chunk;   // strip-rows per CTA (strip-major)
+};
+
+__global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__ ConvParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t acc_full = sbase + BAR_OFF;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 16);
+  if (tid == 0) {
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // weights: OIHW fp32 -> three bf16 parts, UMMA tiles [part][kx][kh] of 160
+  // rows (slice s, co) x 2 K-chunks (8 channels, 16 B), K-major core matrices
+  for (int i = tid; i < 3 * 2 * 2 * NSL * C * 8; i += 128) {
+    const int e = i & 7, co = (i >> 3) % C, s = (i >> 3) / C % NSL;
+    const int kc = (i >> 3) / C / NSL % 2, kh = (i >> 3) / C / NSL / 2 % 2, kx = (i >> 3) / C / NSL / 4;
+    const int ci = kh * 16 + kc * 8 + e, ky = c_ky[s];
+    __nv_bfloat16 w0, w1, w2;
+    split3(P.w[((co * C + ci) * 3 + ky) * 3 + kx], w0, w1, w2);
+    const int off = (kx * 2 + kh) * TILE + kc * (NSL * C * 16) + (s * C + co) * 16 + e * 2;
+    *reinterpret_cast<__nv_bfloat16 *>(smem + off) = w0;
+    *reinterpret_cast<__nv_bfloat16 *>(smem + 6 * TILE + off) = w1;
+    *reinterpret_cast<__nv_bfloat16 *>(smem + 12 * TILE + off) = w2;
+  }
+  for (int i = tid; i < A_BYTES / 16; i += 128)
+    reinterpret_cast<uint4 *>(smem + A_OFF)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);
+  const int l = tid;
+  const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
+  const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)((NSL * C * 16) >> 4) << 16);
+  const size_t plane = (size_t)P.H * P.W;
+  const long long range = P.H;
+  const long long q0 = (long long)blockIdx.x * P.chunk;
+  const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * range);
+  uint32_t ph_acc = 0;
+  float xin[C], vals[C];
+  for (long long qq = q0; qq < q1;) {
+    const int s = (int)(qq / range);
+    const long long end = min(q1, (long long)(s + 1) * range);
+    const int R0 = (int)(qq - (long long)s * range), R1 = (int)(end - (long long)s * range);
+    qq = end;
+    const int A = max(R0 - 1, 0), Bn = min(R1 + 1, P.H);
+    const int v = s * S - 1 + l;
+    const int b = v >= 0 ? v / (P.W + 1) : 0, col = v >= 0 ? v % (P.W + 1) : 0;
+    const bool in_img = v >= 0 && v < P.VW && col < P.W;
+    const bool lane_valid = l >= 1 && l < 1 + S && in_img;
+    const float *xb = P.x + (size_t)b * C * plane + col;
+    auto load_row = [&](int row) {
+#pragma unroll
+      for (int i = 0; i < C; ++i) xin[i] = 0.f;
+      if (in_img && row < Bn) {
+#pragma unroll
+        for (int i = 0; i < C; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
+      }
+    };
+    load_row(A);
+    int tm3 = ((A - 3) % 3 + 3) % 3;   // slot of row r-1 at t = A-2
+    for (int r = A - 2; r <= Bn; ++r) {
+      const int d = r - 1, e = r + 2, slot = tm3;
+      tm3 = tm3 == 2 ? 0 : tm3 + 1;
+      // ---- 1. MMA(r) done (retires every earlier MMA and input buffer)
+      if (r >= A && r < Bn) {
+        if (lane == 0) mbar_wait(acc_full, ph_acc & 1);
+        ph_acc ^= 1u;
+        __syncwarp();
+        tc_fence_after();
+      }
+      // ---- 2. finished output row d -> registers, 3. slot re-init for row e
+      // TMEM: main rings 0..2 (input row mod 3) at 96 q, correction ring at
+      // 288; output row y lives in column block y mod 3 of each ring
+      const uint32_t taddr = tlane + CORR_COL + slot * C;
+      const bool drain = d >= A && d < Bn;
+      if (drain) {
+        tmem_ld32(taddr, vals);
+        // main parts of input rows d-1, d, d+1 (rings x mod 3); an input row
+        // outside [A, Bn) is zero padding: its ring holds an older row
+#pragma unroll
+        for (int k = -1; k <= 1; ++k) {
+          const int xr = d + k;
+          if (xr < A || xr >= Bn) continue;
+          float part[C];
+          tmem_ld32(tlane + (xr % 3) * 3 * C + slot * C, part);
+#pragma unroll
+          for (int i = 0; i < C; ++i) vals[i] += part[i];
+        }
+      }
+      if (e >= A && e < Bn) tmem_st32_zero(taddr);
+      // ---- 4. input row r+1 -> hi / lo A planes, then issue its 36 MMAs
+      const int rn = r + 1;
+      const bool issue = rn >= A && rn < Bn;
+      if (issue) {
+        const int q = rn & 1;
+        const uint32_t dst = sbase + A_OFF + q * NPART * ROW + l * 16;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t w[3][4];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            __nv_bfloat16 a0, a1, a2, c0, c1, c2;
+            split3(xin[8 * g + 2 * k2], a0, a1, a2);
+            split3(xin[8 * g + 2 * k2 + 1], c0, c1, c2);
+            w[0][k2] = pack_bf2(a0, c0);
+            w[1][k2] = pack_bf2(a1, c1);
+            w[2][k2] = pack_bf2(a2, c2);
+          }
+#pragma unroll
+          for (int pp = 0; pp < 3; ++pp)
+            st_shared_v4(dst + pp * ROW + g * PLANE, w[pp][0], w[pp][1], w[pp][2], w[pp][3]);
+        }
+        fence_proxy_async();
+        tmem_wait_st();
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) {
+          tc_fence_after();
+          const int rot = slot == 0 ? 2 : slot - 1;              // (r+1) mod 3
+          const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);       // B window for rows (r+2, r+1, r)
+          const uint64_t a = adesc0 + ((A_OFF + q * NPART * ROW) >> 4);
+          const uint64_t bw = bdesc0 + ((o * C * 16) >> 4);
+          mma36_row(tmem + (uint32_t)((rn % 3) * 3 * C), tmem + CORR_COL, a, a + (ROW >> 4),
+                    a + ((2 * ROW) >> 4), bw, bw + ((6 * TILE) >> 4), bw + ((12 * TILE) >> 4), acc_full);
+          __syncwarp();
+        }
+      }
+      // ---- 5. epilogue of row d (overlaps the MMAs), 6. prefetch the next row
+      if (drain && d >= R0 && d < R1 && lane_valid) {
+        const size_t o0 = (size_t)b * C * plane + (size_t)d * P.W + col;
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const size_t idx = o0 + (size_t)i * plane;
+          float y = vals[i] + (P.bias ? __ldg(P.bias + i) : 0.f);
+          if (P.mask) y = __ldg(P.mask + idx) > 0.f ? y : 0.f;
+          if (P.resid) y += __ldg(P.resid + idx);
+          if (P.relu) y = fmaxf(y, 0.f);
+          P.out[idx] = y;
+        }
+      }
+      if (issue) load_row(rn + 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tct
+
+// x, out, mask, resid: (B, 32, H, W) fp32; w: (32, 32, 3, 3) fp32 OIHW.
+int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+              const float *resid, float *out, int relu, cudaStream_t st) {
+  using namespace tct;
+  static bool attr = false;
+  if (!attr) {
+    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr = true;
+  }
+  int dev = 0, n_sm = 148;
+  HT_CUDA(cudaGetDevice(&dev));
+  HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  ConvParams p{};
+  p.x = x; p.w = w; p.bias = bias; p.mask = mask; p.resid = resid; p.out = out;
+  p.B = B; p.H = H; p.W = W; p.VW = B * (W + 1); p.relu = relu;
+  p.n_strips = (p.VW + S - 1) / S;
+  const long long total = (long long)p.n_strips * H;
+  long long grid = n_sm;
+  if (total < grid * 8) grid = (total + 7) / 8;
+  if (grid < 1) grid = 1;
+  p.chunk = (total + grid - 1) / grid;
+  grid = (total + p.chunk - 1) / p.chunk;
+  conv_tc_kernel<<<(unsigned)grid, 128, SMEM, st>>>(p);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+}  // namespace ht

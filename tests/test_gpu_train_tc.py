@@ -1,0 +1,93 @@
+"""Training convolutions on tcgen05 (split-bf16, csrc/conv_tc.cu) against the fp32
+SIMT kernels and the oracle: forward p and every parameter / input gradient of
+the paper architecture (the golden-vector training tests in test_gpu_train.py
+run on the tensor-core path too, since it is the default)."""
+
+import numpy as np
+import pytest
+
+from paper_2304_12152_b200.imagecore import Rng
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(impl, net, x, dp):
+    import torch
+    from paper_2304_12152_b200 import _lib
+    _lib.call("ht_set_train_conv_impl", impl)
+    try:
+        xd = torch.from_numpy(x.astype(np.float32)).cuda()
+        p = net.forward_device(xd)
+        grad = torch.zeros(net.num_params(), dtype=torch.float64, device="cuda")
+        dx = torch.zeros_like(xd)
+        net.backward_device(torch.from_numpy(dp.astype(np.float32)).cuda(), grad, dx)
+        return p.double().cpu().numpy(), grad.cpu().numpy(), dx.double().cpu().numpy()
+    finally:
+        _lib.call("ht_set_train_conv_impl", 0)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("B,H,W", [(3, 40, 52), (1, 96, 150), (1, 7, 300)])
+def test_tensor_core_training_convs_vs_oracle(B, H, W):
+    """Both the tcgen05 path (impl 0) and the SIMT path (impl 1) against the
+    fp64 oracle: p, parameter gradients per tensor and dx within 1e-4
+    relative, and the tensor-core path (split-bf16, short accumulation chains
+    for the large products: ~1e-7 per conv) no less accurate than SIMT."""
+    from oracle import htoracle as O
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(32, 3)
+    net.init_params(Rng(7), std=0.05)
+    r = Rng(11)
+    x = np.stack([np.stack((r.uniforms(H * W).reshape(H, W), r.gaussians(H * W).reshape(H, W)))
+                  for _ in range(B)]).astype(np.float32).astype(np.float64)
+    dp = (r.gaussians(B * H * W).reshape(B, H, W) * 1e-3).astype(np.float32).astype(np.float64)
+    params = [q.value for q in net.params()]
+    p_ref, cache = O.policy_forward(params, x, keep=True)
+    dx_ref, grads = O.policy_backward(params, cache, dp[:, None])
+    g_ref = np.concatenate([g.ravel() for g in grads])
+    errs = {}
+    for impl in (0, 1):
+        p, g, dx = _run(impl, net, x, dp)
+        assert np.max(np.abs(p - p_ref[:, 0])) < 2e-5
+        at = 0
+        worst = 0.0
+        for t in grads:
+            n = t.size
+            if np.linalg.norm(t) > 0:
+                worst = max(worst, _rel(g[at:at + n], t.ravel()))
+            at += n
+        errs[impl] = (worst, _rel(g, g_ref), _rel(dx, dx_ref))
+        assert worst < 1e-4 and errs[impl][2] < 1e-4, (impl, errs[impl])
+    assert errs[0][1] <= 1.5 * errs[1][1] + 1e-7, errs
+
+
+def test_tensor_core_matches_simt_at_config5_size():
+    """2 x 256^2 (config-5 crops): the two paths agree on p and, normwise, on
+    the gradients to within the cancellation-limited fp32 noise."""
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(32, 3)
+    net.init_params(Rng(7), std=0.05)
+    r = Rng(12)
+    B, H, W = 2, 256, 256
+    x = np.stack([np.stack((r.uniforms(H * W).reshape(H, W), r.gaussians(H * W).reshape(H, W)))
+                  for _ in range(B)])
+    dp = r.gaussians(B * H * W).reshape(B, H, W) * 1e-3
+    p0, g0, dx0 = _run(0, net, x, dp)
+    p1, g1, dx1 = _run(1, net, x, dp)
+    assert np.max(np.abs(p0 - p1)) < 2e-6
+    assert _rel(g0, g1) < 1e-3 and _rel(dx0, dx1) < 1e-3
+
+
+def test_tensor_core_forward_matches_oracle():
+    from oracle import htoracle as O
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(32, 2)
+    net.init_params(Rng(3), std=0.05)
+    r = Rng(5)
+    x = np.stack((r.uniforms(33 * 47).reshape(33, 47), r.gaussians(33 * 47).reshape(33, 47)))[None]
+    p, _, _ = _run(0, net, x, np.zeros((1, 33, 47)))
+    ref = O.policy_forward([q.value for q in net.params()], x.astype(np.float32).astype(np.float64))
+    assert np.max(np.abs(p - ref[:, 0])) < 2e-5
