@@ -69,6 +69,11 @@ int ht_rng_jump(uint64_t state[4], uint64_t n);
  * uniforms of rl.sample_actions (rl.py:67-69). */
 int ht_rng_gaussians_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream);
 int ht_rng_uniforms_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream);
+/* n_maps noise maps of n gaussians in one launch, map m drawn from the stream
+ * state states[4m..4m+3] (host array), written at out + m*n; no host state
+ * advances (the caller recorded the states and jumped past each map). */
+int ht_rng_gaussian_maps_device(const uint64_t *states, int n_maps, int64_t n, void *out, int f64,
+                                void *stream);
 
 /* ---- policy network parameters ----------------------------------------- */
 /* Number of float64 parameters of PolicyNetwork(channels, blocks, in_ch=2). */

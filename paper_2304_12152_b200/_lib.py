@@ -31,6 +31,7 @@ SIGNATURES = {
     "ht_rng_jump": [_u64p, C.c_uint64],
     "ht_rng_gaussians_device": [_u64p, _i64, _vp, _i, _vp],
     "ht_rng_uniforms_device": [_u64p, _i64, _vp, _i, _vp],
+    "ht_rng_gaussian_maps_device": [_vp, _i, _i64, _vp, _i, _vp],
     "ht_num_params": [_i, _i, _i64p],
     "ht_packed_bytes": [_i, _i, _i64p],
     "ht_pack_params": [_vp, _i, _i, _vp, _vp],

@@ -113,14 +113,26 @@ __device__ __forceinline__ double unit(uint64_t x) { return (double)(x >> 11) * 
 
 constexpr int PAIRS_PER_THREAD = 128;
 
-// n gaussians = ceil(n/2) Box-Muller pairs; pair i consumes draws 2i, 2i+1
+// Noise maps of n gaussians each (n gaussians = ceil(n/2) Box-Muller pairs,
+// pair i consuming draws 2i, 2i+1 of its map's stream), map m starting from
+// its own stream state -- maps interleaved with host draws, e.g.
+// rl.train_step's per-sample image pick / crop / noise order, take one
+// launch for all of them; a single stream is the one-map case.
+constexpr int MAX_MAPS = 64;
+struct MapStarts {
+  ulonglong4 s[MAX_MAPS];
+};
+
 template <typename T>
-__global__ void gaussians_kernel(ulonglong4 start, int64_t n, const Mat *__restrict__ J, T *__restrict__ out) {
+__global__ void gaussian_maps_kernel(const __grid_constant__ MapStarts st, int64_t n, const Mat *__restrict__ J,
+                                     T *__restrict__ out) {
   const int64_t npairs = (n + 1) / 2;
   const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * PAIRS_PER_THREAD;
   if (p0 >= npairs) return;
-  uint64_t s[4] = {start.x, start.y, start.z, start.w};
+  const ulonglong4 s0 = st.s[blockIdx.y];
+  uint64_t s[4] = {s0.x, s0.y, s0.z, s0.w};
   jump_dev(J, s, 2ull * (uint64_t)p0);
+  T *o = out + (int64_t)blockIdx.y * n;
   const int64_t p1 = min(npairs, p0 + PAIRS_PER_THREAD);
   const double two_pi = 2.0 * 3.14159265358979323846;
   for (int64_t p = p0; p < p1; ++p) {
@@ -129,9 +141,32 @@ __global__ void gaussians_kernel(ulonglong4 start, int64_t n, const Mat *__restr
     const double r = sqrt(-2.0 * log(1.0 - u0));
     double sn, cs;
     sincos(two_pi * u1, &sn, &cs);
-    out[2 * p] = (T)(r * cs);
-    if (2 * p + 1 < n) out[2 * p + 1] = (T)(r * sn);
+    o[2 * p] = (T)(r * cs);
+    if (2 * p + 1 < n) o[2 * p + 1] = (T)(r * sn);
   }
+}
+
+template <typename T>
+static int launch_maps(const uint64_t *states, int n_maps, int64_t n, T *out, cudaStream_t st) {
+  HT_REQUIRE(n_maps >= 0 && n >= 0, "counts must be non-negative");
+  if (n_maps == 0 || n == 0) return HT_OK;
+  const Mat *J = device_tables();
+  HT_REQUIRE(J != nullptr, "could not upload RNG jump tables");
+  const int threads = 128;
+  const int64_t units = ((n + 1) / 2 + PAIRS_PER_THREAD - 1) / PAIRS_PER_THREAD;
+  const int64_t blocks = (units + threads - 1) / threads;
+  HT_REQUIRE(blocks < (1ll << 31), "too many draws");
+  for (int m0 = 0; m0 < n_maps; m0 += MAX_MAPS) {
+    MapStarts ms{};
+    const int cnt = min(MAX_MAPS, n_maps - m0);
+    for (int m = 0; m < cnt; ++m)
+      ms.s[m] = make_ulonglong4(states[4 * (m0 + m)], states[4 * (m0 + m) + 1], states[4 * (m0 + m) + 2],
+                                states[4 * (m0 + m) + 3]);
+    gaussian_maps_kernel<T><<<dim3((unsigned)blocks, (unsigned)cnt), threads, 0, st>>>(ms, n, J, out + (int64_t)m0 * n);
+    count_launch();
+    HT_CHECK_LAUNCH();
+  }
+  return HT_OK;
 }
 
 constexpr int DRAWS_PER_THREAD = 256;
@@ -146,24 +181,29 @@ __global__ void uniforms_kernel(ulonglong4 start, int64_t n, const Mat *__restri
   for (int64_t i = i0; i < i1; ++i) out[i] = (T)unit(next_dev(s));
 }
 
-template <typename T, bool GAUSS>
-static int launch(uint64_t state[4], int64_t n, T *out, cudaStream_t st) {
+template <typename T>
+static int launch_uniforms(uint64_t state[4], int64_t n, T *out, cudaStream_t st) {
   HT_REQUIRE(n >= 0, "n must be non-negative");
   if (n == 0) return HT_OK;
   const Mat *J = device_tables();
   HT_REQUIRE(J != nullptr, "could not upload RNG jump tables");
   const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
-  const int64_t units = GAUSS ? ((n + 1) / 2 + PAIRS_PER_THREAD - 1) / PAIRS_PER_THREAD
-                              : (n + DRAWS_PER_THREAD - 1) / DRAWS_PER_THREAD;
   const int threads = 128;
-  const int64_t blocks = (units + threads - 1) / threads;
+  const int64_t blocks = ((n + DRAWS_PER_THREAD - 1) / DRAWS_PER_THREAD + threads - 1) / threads;
   HT_REQUIRE(blocks < (1ll << 31), "too many draws");
-  if (GAUSS) gaussians_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(s0, n, J, out);
-  else uniforms_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(s0, n, J, out);
+  uniforms_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(s0, n, J, out);
   count_launch();
   HT_CHECK_LAUNCH();
-  jump_host(state, GAUSS ? 2ull * (uint64_t)((n + 1) / 2) : (uint64_t)n);
+  jump_host(state, (uint64_t)n);
   return HT_OK;
+}
+
+template <typename T>
+static int launch_gaussians(uint64_t state[4], int64_t n, T *out, cudaStream_t st) {
+  HT_REQUIRE(n >= 0, "n must be non-negative");
+  const int rc = launch_maps<T>(state, 1, n, out, st);
+  if (rc == HT_OK) jump_host(state, 2ull * (uint64_t)((n + 1) / 2));
+  return rc;
 }
 
 }  // namespace rng
@@ -179,12 +219,19 @@ int ht_rng_jump(uint64_t state[4], uint64_t n) {
 // Device Rng.gaussians / Rng.uniforms: out is a device pointer; the host
 // state advances exactly as the host functions would.
 int ht_rng_gaussians_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream) {
-  return f64 ? ht::rng::launch<double, true>(state, n, (double *)out, (cudaStream_t)stream)
-             : ht::rng::launch<float, true>(state, n, (float *)out, (cudaStream_t)stream);
+  return f64 ? ht::rng::launch_gaussians<double>(state, n, (double *)out, (cudaStream_t)stream)
+             : ht::rng::launch_gaussians<float>(state, n, (float *)out, (cudaStream_t)stream);
+}
+// n_maps noise maps of n gaussians, map m drawn from stream state
+// states[4m..4m+3] (host array); no host state is advanced.
+int ht_rng_gaussian_maps_device(const uint64_t *states, int n_maps, int64_t n, void *out, int f64,
+                                void *stream) {
+  return f64 ? ht::rng::launch_maps<double>(states, n_maps, n, (double *)out, (cudaStream_t)stream)
+             : ht::rng::launch_maps<float>(states, n_maps, n, (float *)out, (cudaStream_t)stream);
 }
 int ht_rng_uniforms_device(uint64_t state[4], int64_t n, void *out, int f64, void *stream) {
-  return f64 ? ht::rng::launch<double, false>(state, n, (double *)out, (cudaStream_t)stream)
-             : ht::rng::launch<float, false>(state, n, (float *)out, (cudaStream_t)stream);
+  return f64 ? ht::rng::launch_uniforms<double>(state, n, (double *)out, (cudaStream_t)stream)
+             : ht::rng::launch_uniforms<float>(state, n, (float *)out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -156,6 +156,24 @@ def gaussian_noise_map_device(rng, width, height, dtype=None, device=None):
     return rng.gaussians_device(width * height, dtype=dtype, device=device).view(height, width)
 
 
+def gaussian_maps_device(states, width, height, dtype=None, device=None):
+    """Noise maps drawn on the GPU in one launch, map m from the stream state
+    states[m] (4 words, as recorded with Rng.state_words() before the map's
+    draws).  Returns a (len(states), height, width) CUDA tensor."""
+    import torch
+    _lib.require_cuda()
+    n_maps = len(states)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((n_maps, height, width), dtype=dtype or torch.float32, device=dev)
+    if n_maps:
+        words = np.ascontiguousarray(np.array(states, dtype=np.uint64).reshape(n_maps, 4))
+        with torch.cuda.device(dev):
+            _lib.call("ht_rng_gaussian_maps_device", words.ctypes.data_as(C.c_void_p), n_maps,
+                      C.c_int64(width * height), _lib.ptr(out), int(out.dtype == torch.float64),
+                      _lib.stream_ptr())
+    return out
+
+
 def constant_image(gray, width, height):
     """imagecore.py:146-152."""
     if not 0.0 <= gray <= 1.0:

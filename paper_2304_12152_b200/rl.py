@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _lib
 from .hvs import HvsConfig
-from .imagecore import Rng, gaussian_noise_map, gaussian_noise_map_device, random_crop
+from .imagecore import (Rng, gaussian_maps_device, gaussian_noise_map, gaussian_noise_map_device,
+                        random_crop)
 from .metrics import MetricConfig, reinforce_signal_device, reward, reward_signal_device
 from .nn import Adam, PolicyNetwork, cosine_lr, load_checkpoint
 from .spectral import anisotropy_device, ring_partition
@@ -237,22 +238,26 @@ from .parallel import dist_info as _dist_info  # noqa: E402
 
 def draw_batch(dataset, cfg, rng, device=None, keep=None):
     """RNG draws of rl.py:242-245 in reference order (image pick, crop y,
-    crop x, noise map).  With `device`, noise maps are drawn on the GPU;
-    samples outside `keep` (a range: another rank's shard) only advance the
-    stream past their noise (jump-ahead) and get None."""
+    crop x, noise map).  Host mode returns (crops, noise maps).  With
+    `device`, the noise maps of the samples in `keep` (a range: this rank's
+    shard) are drawn on the GPU in one launch from the stream states they
+    start at, the others only advance the stream (jump-ahead); returns
+    (crops, (len(keep), size, size) float32 CUDA tensor)."""
     size = cfg.crop_size
-    crops, noises = [], []
+    draws = 2 * ((size * size + 1) // 2)          # one gaussian_noise_map
+    crops, noises, starts = [], [], []
     for i in range(cfg.batch_size):
         img = dataset[rng.randint(len(dataset))]
         crops.append(random_crop(rng, img, size))
         if device is None:
             noises.append(gaussian_noise_map(rng, size, size))
-        elif keep is None or i in keep:
-            noises.append(gaussian_noise_map_device(rng, size, size, device=device))
         else:
-            rng.jump(2 * ((size * size + 1) // 2))
-            noises.append(None)
-    return crops, noises
+            if keep is None or i in keep:
+                starts.append(rng.state_words())
+            rng.jump(draws)
+    if device is None:
+        return crops, noises
+    return crops, gaussian_maps_device(starts, size, size, device=device)
 
 
 def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None):
@@ -275,19 +280,16 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     p = None
     if hi > lo:
         cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).to(dev)
-        zd = torch.stack(noises[lo:hi])
-        p = net.forward_device(torch.stack((cd, zd), dim=1))
-    # action uniforms for every sample, in order (rl.py:249 -> rl.py:68),
-    # drawn on the GPU for this rank's shard, skipped (jump) for the others
-    us = []
-    for i in range(bs):
-        if lo <= i < hi:
-            us.append(rng.uniforms_device(size * size, device=dev).view(size, size))
-        else:
-            rng.jump(size * size)
+        p = net.forward_device(torch.stack((cd, noises), dim=1))
+    # action uniforms for every sample, in order (rl.py:249 -> rl.py:68): this
+    # rank's shard is one contiguous stretch of the stream, drawn on the GPU
+    # in one launch; the other ranks' stretches are skipped (jump-ahead)
+    n = size * size
+    rng.jump(lo * n)
+    ud = rng.uniforms_device((hi - lo) * n, device=dev).view(hi - lo, size, size) if hi > lo else None
+    rng.jump((bs - hi) * n)
     reinforce = cfg.estimator in ("reinforce", "reinforce_meanbaseline")
     if hi > lo:
-        ud = torch.stack(us)
         if not reinforce:
             m, sig, rew = reward_signal_device(p, ud, cd, mcfg, scale=1.0 / bs, levels=cfg.levels,
                                                estimator=cfg.estimator)
@@ -317,16 +319,19 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
         ba = cfg.anisotropy_batch_size or bs
         grays = [rng.uniform() for _ in range(ba)]
         glo, ghi = shard_range(ba, rank, world)
-        znoise = []
+        # the gray images' noise maps follow each other in the stream: this
+        # rank's maps in one launch from their start states, the rest skipped
+        draws = 2 * ((size * size + 1) // 2)
+        starts = []
         for i in range(ba):
             if glo <= i < ghi:
-                znoise.append(gaussian_noise_map_device(rng, size, size, device=dev))
-            else:
-                rng.jump(2 * ((size * size + 1) // 2))
+                starts.append(rng.state_words())
+            rng.jump(draws)
         if ghi > glo:
+            znoise = gaussian_maps_device(starts, size, size, device=dev)
             gd = torch.tensor([grays[i] for i in range(glo, ghi)], dtype=torch.float64)
             gd = gd.to(torch.float32).to(dev)[:, None, None].expand(-1, size, size)
-            pg = net.forward_device(torch.stack((gd, torch.stack(znoise)), dim=1).contiguous())
+            pg = net.forward_device(torch.stack((gd, znoise), dim=1).contiguous())
             part = _part_cache(size)
             loss, dpg = anisotropy_device(pg, part, scale=cfg.w_a / ba)
             net.backward_device(dpg, grad)

@@ -102,3 +102,28 @@ def test_print_page_noise_is_fast():
     dt = time.perf_counter() - t
     assert z.shape == (7016, 4960) and dt < 0.1
     assert abs(float(z.mean())) < 1e-3 and abs(float(z.std()) - 1.0) < 1e-3
+
+
+@pytest.mark.gpu
+def test_gaussian_maps_from_recorded_states():
+    """One launch for maps interleaved with host draws (rl.draw_batch order):
+    map m equals the single-stream draw from the state it starts at."""
+    import torch
+    from paper_2304_12152_b200.imagecore import gaussian_maps_device
+    r = Rng(77)
+    starts, singles = [], []
+    for i in range(5):
+        r.randint(7)                               # host draws between maps
+        starts.append(r.state_words())
+        s = Rng(0)
+        s.set_state_words(r.state_words())
+        singles.append(s.gaussians_device(30 * 41).cpu().numpy().reshape(30, 41))
+        r.jump(2 * ((30 * 41 + 1) // 2))
+    maps = gaussian_maps_device(starts, 41, 30).cpu().numpy()
+    assert maps.shape == (5, 30, 41)
+    assert np.array_equal(maps, np.stack(singles))
+    host = Rng(0)
+    host.set_state_words(starts[3])
+    f = host.gaussians_f32(30 * 41).reshape(30, 41)
+    assert np.mean(maps[3] != f) <= 1e-3
+    assert gaussian_maps_device([], 4, 4).shape == (0, 4, 4)
