@@ -24,7 +24,8 @@
 //   6 split products);
 // * one CTA per SM: the weights (three bf16 parts, 90 KB) are split into
 //   UMMA tiles by every CTA from the OIHW fp32 tensor, two input rows (three
-//   parts, 48 KB) are double buffered; 4 warps, thread = pixel lane.
+//   parts, 48 KB) are double buffered; 8 warps, thread = (pixel lane,
+//   16-channel half).
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -49,6 +50,8 @@ constexpr int A_BYTES = 2 * NPART * ROW;    // 2 buffers x 3 parts
 constexpr int BAR_OFF = A_OFF + A_BYTES;
 constexpr int SMEM = BAR_OFF + 16 + 16;
 constexpr int CORR_COL = 3 * 3 * C;   // TMEM column of the correction ring
+constexpr int NTHR = 256;             // 2 channel halves x 4 lane quarters
+constexpr int HC = C / 2;             // channels per thread
 constexpr uint32_t IDESC_BF16 =
     (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 __constant__ int c_ky[NSL] = {2, 1, 0, 2, 1};
@@ -165,7 +168,7 @@ struct ConvParams {
   long long chunk;   // strip-rows per CTA (strip-major)
 };
 
-__global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__ ConvParams P) {
+__global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant__ ConvParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
   }
   // weights: OIHW fp32 -> three bf16 parts, UMMA tiles [part][kx][kh] of 160
   // rows (slice s, co) x 2 K-chunks (8 channels, 16 B), K-major core matrices
-  for (int i = tid; i < 3 * 2 * 2 * NSL * C * 8; i += 128) {
+  for (int i = tid; i < 3 * 2 * 2 * NSL * C * 8; i += NTHR) {
     const int e = i & 7, co = (i >> 3) % C, s = (i >> 3) / C % NSL;
     const int kc = (i >> 3) / C / NSL % 2, kh = (i >> 3) / C / NSL / 2 % 2, kx = (i >> 3) / C / NSL / 4;
     const int ci = kh * 16 + kc * 8 + e, ky = c_ky[s];
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
     *reinterpret_cast<__nv_bfloat16 *>(smem + 6 * TILE + off) = w1;
     *reinterpret_cast<__nv_bfloat16 *>(smem + 12 * TILE + off) = w2;
   }
-  for (int i = tid; i < A_BYTES / 16; i += 128)
+  for (int i = tid; i < A_BYTES / 16; i += NTHR)
     reinterpret_cast<uint4 *>(smem + A_OFF)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async();
   if (warp == 0) {
@@ -200,8 +203,13 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);
-  const int l = tid;
+  // two warpgroups: warp w serves TMEM lane quarter w & 3 (pixel lanes) and
+  // channel half w >> 2 (16 channels) -- twice the warps of one pixel per
+  // thread, for the epilogue's and loader's memory latency
+  const int wq = warp & 3, half = warp >> 2;
+  const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16);
+  const int l = wq * 32 + lane;
+  const int c0 = half * HC;
   const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
   const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)((NSL * C * 16) >> 4) << 16);
   const size_t plane = (size_t)P.H * P.W;
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
   const long long q0 = (long long)blockIdx.x * P.chunk;
   const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * range);
   uint32_t ph_acc = 0;
-  float xin[C], vals[C];
+  float xin[HC], vals[HC];
   for (long long qq = q0; qq < q1;) {
     const int s = (int)(qq / range);
     const long long end = min(q1, (long long)(s + 1) * range);
@@ -220,13 +228,13 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
     const int b = v >= 0 ? v / (P.W + 1) : 0, col = v >= 0 ? v % (P.W + 1) : 0;
     const bool in_img = v >= 0 && v < P.VW && col < P.W;
     const bool lane_valid = l >= 1 && l < 1 + S && in_img;
-    const float *xb = P.x + (size_t)b * C * plane + col;
+    const float *xb = P.x + ((size_t)b * C + c0) * plane + col;
     auto load_row = [&](int row) {
 #pragma unroll
-      for (int i = 0; i < C; ++i) xin[i] = 0.f;
+      for (int i = 0; i < HC; ++i) xin[i] = 0.f;
       if (in_img && row < Bn) {
 #pragma unroll
-        for (int i = 0; i < C; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
+        for (int i = 0; i < HC; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
       }
     };
     load_row(A);
@@ -244,31 +252,31 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
       // ---- 2. finished output row d -> registers, 3. slot re-init for row e
       // TMEM: main rings 0..2 (input row mod 3) at 96 q, correction ring at
       // 288; output row y lives in column block y mod 3 of each ring
-      const uint32_t taddr = tlane + CORR_COL + slot * C;
+      const uint32_t taddr = tlane + CORR_COL + slot * C + c0;
       const bool drain = d >= A && d < Bn;
       if (drain) {
-        tmem_ld32(taddr, vals);
+        tmem_ld16(taddr, vals);
         // main parts of input rows d-1, d, d+1 (rings x mod 3); an input row
         // outside [A, Bn) is zero padding: its ring holds an older row
 #pragma unroll
         for (int k = -1; k <= 1; ++k) {
           const int xr = d + k;
           if (xr < A || xr >= Bn) continue;
-          float part[C];
-          tmem_ld32(tlane + (xr % 3) * 3 * C + slot * C, part);
+          float part[HC];
+          tmem_ld16(tlane + (xr % 3) * 3 * C + slot * C + c0, part);
 #pragma unroll
-          for (int i = 0; i < C; ++i) vals[i] += part[i];
+          for (int i = 0; i < HC; ++i) vals[i] += part[i];
         }
       }
-      if (e >= A && e < Bn) tmem_st32_zero(taddr);
+      if (e >= A && e < Bn) tmem_st16_zero(taddr);
       // ---- 4. input row r+1 -> hi / lo A planes, then issue its 36 MMAs
       const int rn = r + 1;
       const bool issue = rn >= A && rn < Bn;
       if (issue) {
         const int q = rn & 1;
-        const uint32_t dst = sbase + A_OFF + q * NPART * ROW + l * 16;
+        const uint32_t dst = sbase + A_OFF + q * NPART * ROW + (2 * half) * PLANE + l * 16;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           uint32_t w[3][4];
 #pragma unroll
           for (int k2 = 0; k2 < 4; ++k2) {
@@ -300,11 +308,11 @@ __global__ void __launch_bounds__(128, 1) conv_tc_kernel(const __grid_constant__
       }
       // ---- 5. epilogue of row d (overlaps the MMAs), 6. prefetch the next row
       if (drain && d >= R0 && d < R1 && lane_valid) {
-        const size_t o0 = (size_t)b * C * plane + (size_t)d * P.W + col;
+        const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
 #pragma unroll
-        for (int i = 0; i < C; ++i) {
+        for (int i = 0; i < HC; ++i) {
           const size_t idx = o0 + (size_t)i * plane;
-          float y = vals[i] + (P.bias ? __ldg(P.bias + i) : 0.f);
+          float y = vals[i] + (P.bias ? __ldg(P.bias + c0 + i) : 0.f);
           if (P.mask) y = __ldg(P.mask + idx) > 0.f ? y : 0.f;
           if (P.resid) y += __ldg(P.resid + idx);
           if (P.relu) y = fmaxf(y, 0.f);
@@ -346,7 +354,7 @@ int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *
   if (grid < 1) grid = 1;
   p.chunk = (total + grid - 1) / grid;
   grid = (total + p.chunk - 1) / p.chunk;
-  conv_tc_kernel<<<(unsigned)grid, 128, SMEM, st>>>(p);
+  conv_tc_kernel<<<(unsigned)grid, NTHR, SMEM, st>>>(p);
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
