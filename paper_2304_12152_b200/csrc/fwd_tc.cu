@@ -342,11 +342,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
       auto load_row32 = [&](int row, float (&dst)[32]) {   // fp32 x row (0 outside)
 #pragma unroll
         for (int i = 0; i < 32; ++i) dst[i] = 0.f;
-#ifdef HT_KO_GLOAD
-        if (false) {
-#else
         if (row < Bn && v >= 0 && v < P.VW) {
-#endif
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             const float4 f = ldg_stream(reinterpret_cast<const float4 *>(P.x_in) + xoff(row, g));
@@ -426,9 +422,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
 #pragma unroll
               for (int i = 0; i < 32; ++i) resbuf[i] += PBIAS(j, i);
               tmem_st32(taddr, resbuf);
-#ifndef HT_KO_GRES
               if constexpr (GRES) advance(e + 1);
-#endif
             }
           } else if constexpr (kind == K_OUT) {
             tmem_st16_zero(taddr);
@@ -556,13 +550,8 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
             }
             PROF_MARK(10);
             const uint32_t dst = sbase + PL::a_off(j + 1) + q * PL::abytes(j + 1) + (l + 1) * 16;
-#ifndef HT_KO_STS
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)
-#else
-            if (hv[0] == 12345u)
-            for (int c4 = 0; c4 < 4; ++c4)
-#endif
               st_shared_v4(dst + c4 * PLANE, hv[4 * c4], hv[4 * c4 + 1], hv[4 * c4 + 2], hv[4 * c4 + 3]);
             PROF_MARK(11);
             fence_proxy_async();
@@ -572,11 +561,7 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
             PROF_MARK(13);
           } else {
             // last layer of a non-output pass: fp32 x -> global
-#ifdef HT_KO_GSTORE
-            if (vals[0] == 12345.f) {
-#else
             if (lane_valid && d >= R0 && d < R1) {
-#endif
               float4 *dstg = reinterpret_cast<float4 *>(P.x_out);
 #pragma unroll
               for (int g = 0; g < 8; ++g)
