@@ -214,7 +214,94 @@ __global__ void threshold_window_kernel(const float *__restrict__ logit, int B, 
 // host orchestration
 namespace ht {
 
-// conv_tc.cu: the 32 -> 32 training conv on tcgen05 (3xTF32)
+// wgrad for the 32 -> 32 convs (the dominant training kernel): thread =
+// (ci, ky) with all three kx taps x 32 co in registers, a sliding window
+// over the x row (one shared load per pixel for 96 FMAs) and dout read as
+// broadcast 16-B loads from pixel rows padded to 36 floats (conflict-light
+// transposing stores of the coalesced NCHW loads).
+constexpr int W32_NT = 96, W32_PAD = 36;
+constexpr int W32_TX = 32, W32_TY = 8;   // 256-pixel tiles (measured faster than 128: per-tile overhead)
+
+__global__ void __launch_bounds__(W32_NT)
+conv3x3_wgrad32_kernel(const float *__restrict__ x, const float *__restrict__ dout, int B, int H, int W,
+                       int tiles_per_cta, double *__restrict__ dw, double *__restrict__ db) {
+  constexpr int C = 32, TXP = W32_TX + 2, TYP = W32_TY + 2, NP = W32_TY * W32_TX;
+  extern __shared__ float smem[];
+  float *xs = smem;                       // [C][TYP][TXP]
+  float *ds = smem + C * TYP * TXP;       // [NP][W32_PAD]
+  const int tid = threadIdx.x;
+  const int ci = tid / 3, ky = tid % 3;
+  float acc[3][C];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < C; ++j) acc[k][j] = 0.f;
+  float bacc = 0.f;
+  const int tx_n = (W + W32_TX - 1) / W32_TX, ty_n = (H + W32_TY - 1) / W32_TY;
+  const long total_tiles = (long)B * tx_n * ty_n;
+  const size_t plane = (size_t)H * W;
+  for (int it = 0; it < tiles_per_cta; ++it) {
+    const long t = (long)blockIdx.x * tiles_per_cta + it;
+    if (t >= total_tiles) break;
+    const int b = (int)(t / (tx_n * ty_n));
+    const int rem = (int)(t % (tx_n * ty_n));
+    const int y0 = (rem / tx_n) * W32_TY, x0 = (rem % tx_n) * W32_TX;
+    __syncthreads();
+    for (int i = tid; i < C * TYP * TXP; i += W32_NT) {
+      const int c = i / (TYP * TXP), r = i % (TYP * TXP);
+      const int yy = r / TXP, xx = r % TXP;
+      const int gy = y0 + yy - 1, gx = x0 + xx - 1;
+      xs[i] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? x[((size_t)b * C + c) * plane + (size_t)gy * W + gx] : 0.f;
+    }
+    // dout tile: consecutive threads = consecutive pixels (coalesced), four
+    // channels per thread -> one 16-B store into the pixel's padded row
+    for (int i = tid; i < NP * (C / 4); i += W32_NT) {
+      const int pp = i % NP, cg = i / NP;
+      const int gy = y0 + pp / W32_TX, gx = x0 + pp % W32_TX;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gy < H && gx < W) {
+        const float *src = dout + ((size_t)b * C + 4 * cg) * plane + (size_t)gy * W + gx;
+        v = make_float4(src[0], src[plane], src[2 * plane], src[3 * plane]);
+      }
+      *reinterpret_cast<float4 *>(ds + pp * W32_PAD + 4 * cg) = v;
+    }
+    __syncthreads();
+    const float *xr = xs + (ci * TYP + ky) * TXP;
+#pragma unroll 1
+    for (int yy = 0; yy < W32_TY; ++yy) {
+      const float *row = xr + yy * TXP;
+      float xa = row[0], xb = row[1];
+#pragma unroll 2
+      for (int xx = 0; xx < W32_TX; ++xx) {
+        const float xc = row[xx + 2];
+        const float4 *dr = reinterpret_cast<const float4 *>(ds + (yy * W32_TX + xx) * W32_PAD);
+#pragma unroll
+        for (int q = 0; q < C / 4; ++q) {
+          const float4 d = dr[q];
+          const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc[0][4 * q + k] = fmaf(dv[k], xa, acc[0][4 * q + k]);
+            acc[1][4 * q + k] = fmaf(dv[k], xb, acc[1][4 * q + k]);
+            acc[2][4 * q + k] = fmaf(dv[k], xc, acc[2][4 * q + k]);
+          }
+        }
+        xa = xb;
+        xb = xc;
+      }
+    }
+    if (tid < C) {
+      for (int pp = 0; pp < NP; ++pp) bacc += ds[pp * W32_PAD + tid];
+    }
+  }
+#pragma unroll
+  for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+    for (int co = 0; co < C; ++co) atomicAdd(&dw[((size_t)(co * C + ci) * 3 + ky) * 3 + kx], (double)acc[kx][co]);
+  if (tid < C) atomicAdd(&db[tid], (double)bacc);
+}
+
+// conv_tc.cu: the 32 -> 32 training conv on tcgen05 (split-bf16, fp32-level)
 int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
               const float *resid, float *out, int relu, cudaStream_t st);
 extern int g_train_conv_impl;   // 0: tensor cores for 32 -> 32 convs (default), 1: SIMT only
@@ -236,6 +323,22 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
 template <int CIN, int COUT>
 static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, double *dw,
                       double *db, cudaStream_t st) {
+  if constexpr (CIN == 32 && COUT == 32) {
+    const size_t smem = sizeof(float) * ((size_t)32 * (W32_TY + 2) * (W32_TX + 2) + W32_TY * W32_TX * W32_PAD);
+    static bool attr32 = false;
+    if (!attr32) {
+      HT_CUDA(cudaFuncSetAttribute(conv3x3_wgrad32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr32 = true;
+    }
+    const long tiles = (long)B * ((W + W32_TX - 1) / W32_TX) * ((H + W32_TY - 1) / W32_TY);
+    const int per = tiles > 148 * 2 ? (int)((tiles + 148 * 2 - 1) / (148 * 2)) : 1;
+    const int grid = (int)((tiles + per - 1) / per);
+    conv3x3_wgrad32_kernel<<<grid, W32_NT, smem, st>>>(x, dout, B, H, W, per, dw, db);
+    count_launch();
+    HT_CHECK_LAUNCH();
+    return HT_OK;
+  }
   constexpr int NT = CIN * 9 < 64 ? 64 : CIN * 9;
   const size_t smem = sizeof(float) * ((size_t)CIN * (WT_Y + 2) * (WT_X + 2) + WT_Y * WT_X * COUT);
   static bool attr_set = false;
