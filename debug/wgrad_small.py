@@ -1,0 +1,11 @@
+import ctypes as C, sys, torch
+sys.path.insert(0, '.')
+from paper_2304_12152_b200 import _lib
+B, H, W = 1, 4, 32
+x = torch.randn(B, 32, H, W, device='cuda'); d = torch.randn(B, 32, H, W, device='cuda')
+dw = torch.zeros(9216, dtype=torch.float64, device='cuda'); db = torch.zeros(32, dtype=torch.float64, device='cuda')
+parts = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+_lib.call("ht_wgrad3x3_32", C.c_void_p(x.data_ptr()), C.c_void_p(d.data_ptr()), B, H, W,
+          C.c_void_p(dw.data_ptr()), C.c_void_p(db.data_ptr()), 0, parts, None)
+torch.cuda.synchronize()
+print("ok", dw.abs().sum().item())

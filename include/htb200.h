@@ -133,9 +133,13 @@ int ht_timing_enable(int on);
 int ht_timing_read(int *tags, float *ms, int max, int *count);
 
 /* Training convolutions (nn.py:46-77): 0 = the 32 -> 32 convs of the residual
- * blocks (forward and input-gradient) on tcgen05 with 3xTF32 operands
- * (default), 1 = fp32 SIMT kernels only (cross-check).  Process-wide. */
+ * blocks (forward, input gradient and weight gradient) on tcgen05 with
+ * split-bf16 operands (default), 1 = fp32 SIMT kernels only (cross-check).
+ * Process-wide. */
 int ht_set_train_conv_impl(int impl);
+/* bf16 parts of the tensor-core weight gradient: 3 (six products, fp32
+ * level; default) or 2 (three products, ~2^-16 per product). */
+int ht_set_wgrad_parts(int parts);
 /* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
  * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +
  * bias, zeroed where mask <= 0, + resid, ReLU if relu -- Conv2d.forward
@@ -144,19 +148,31 @@ int ht_set_train_conv_impl(int impl);
 int ht_conv3x3_32(const float *x, int B, int H, int W, const float *w, const float *bias,
                   const float *mask, const float *resid, float *out, int relu, int impl,
                   void *stream);
+/* Weight / bias gradient of one such convolution (Conv2d.backward's dW, db,
+ * nn.py:62-77): dw (32,32,3,3) and db (32) fp64 are accumulated into (+=);
+ * impl 0 = tcgen05 with `parts` bf16 parts (2 or 3), 1 = fp32 SIMT. */
+int ht_wgrad3x3_32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db,
+                   int impl, int parts, void *stream);
 
 /* ---- K1' / K2: training forward (stores activations) and backward -------
  * Replaces PolicyNetwork.forward/backward (nn.py:138-160) incl.
  * ResidualBlock (nn.py:91-100) and Conv2d (nn.py:46-77), fp32 math.
  * x_dev: (B, 2, H, W) float32.  act_dev: ht_train_act_bytes() bytes.
  * p_dev: (B, H, W) float32 output.  Returns HT_E_NONFINITE on non-finite
- * logits (nn.py:147-148).  The 32 -> 32 convs run on tcgen05 (3xTF32), the
- * rest in fp32 SIMT (see ht_set_train_conv_impl). */
+ * logits (nn.py:147-148).  The 32 -> 32 convs run on tcgen05 (split bf16),
+ * the rest in fp32 SIMT (see ht_set_train_conv_impl). */
 int ht_train_act_bytes(int channels, int blocks, int B, int H, int W,
                        int64_t *bytes);
 int ht_policy_forward_train(const void *packed_dev, int channels, int blocks,
                             const float *x_dev, int B, int H, int W,
                             void *act_dev, float *p_dev, void *stream);
+/* Same without waiting for the GPU: non-finite logits are OR'ed into
+ * *flag_dev (a device int the caller zeroes and checks later -- rl.train_step
+ * checks it once per step, before the parameter update, and raises as
+ * nn.py:147-148 would). */
+int ht_policy_forward_train_async(const void *packed_dev, int channels, int blocks,
+                                  const float *x_dev, int B, int H, int W,
+                                  void *act_dev, float *p_dev, int *flag_dev, void *stream);
 /* dp_dev (B,H,W) float32 = dL/dp injected at the sigmoid output.
  * grad_dev: flat float64 gradient in params() order, ACCUMULATED (+=) like
  * the reference's .grad (nn.py:66-73; caller zeroes, nn.py:134-136).

@@ -45,9 +45,12 @@ SIGNATURES = {
     "ht_timing_enable": [_i],
     "ht_timing_read": [_vp, _vp, _i, _ip],
     "ht_set_train_conv_impl": [_i],
+    "ht_set_wgrad_parts": [_i],
+    "ht_wgrad3x3_32": [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _vp],
     "ht_conv3x3_32": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "ht_train_act_bytes": [_i, _i, _i, _i, _i, _i64p],
     "ht_policy_forward_train": [_vp, _i, _i, _vp, _i, _i, _i, _vp, _vp, _vp],
+    "ht_policy_forward_train_async": [_vp, _i, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp],
     "ht_policy_backward": [_vp, _i, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "ht_reward_workspace_bytes": [_i, _i, _i, _i64p],
     "ht_reward_le": [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _d, _d, _d, _d, _d, _vp, _vp,

@@ -62,6 +62,7 @@ void timing_mark_end(cudaStream_t st) {
 }
 
 int g_train_conv_impl = 0;
+int g_wgrad_parts = 3;
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
 static inline uint64_t splitmix64(uint64_t &s) {
@@ -123,11 +124,17 @@ int ht_timing_read(int *tags, float *ms, int max, int *count) {
   return HT_OK;
 }
 
-// Training convolutions: 0 = tcgen05 3xTF32 kernel for the 32 -> 32 convs
-// (default), 1 = fp32 SIMT kernels only (cross-check).
+// Training convolutions: 0 = tcgen05 split-bf16 kernels for the 32 -> 32
+// convs (default), 1 = fp32 SIMT kernels only (cross-check).
 int ht_set_train_conv_impl(int impl) {
   if (impl != 0 && impl != 1) return ht::fail(HT_E_INVALID, "impl must be 0 (tensor core) or 1 (simt)");
   ht::g_train_conv_impl = impl;
+  return HT_OK;
+}
+
+int ht_set_wgrad_parts(int parts) {
+  if (parts != 2 && parts != 3) return ht::fail(HT_E_INVALID, "parts must be 2 or 3");
+  ht::g_wgrad_parts = parts;
   return HT_OK;
 }
 

@@ -305,6 +305,10 @@ conv3x3_wgrad32_kernel(const float *__restrict__ x, const float *__restrict__ do
 int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
               const float *resid, float *out, int relu, cudaStream_t st);
 extern int g_train_conv_impl;   // 0: tensor cores for 32 -> 32 convs (default), 1: SIMT only
+// wgrad_tc.cu: their weight gradient on tcgen05 (split-bf16, `parts` bf16 parts)
+int wgrad_tc32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int parts,
+               cudaStream_t st);
+extern int g_wgrad_parts;
 
 template <int CIN, int COUT>
 static int conv_fwd(const float *x, int B, int H, int W, const float *w, const float *bias,
@@ -324,6 +328,8 @@ template <int CIN, int COUT>
 static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, double *dw,
                       double *db, cudaStream_t st) {
   if constexpr (CIN == 32 && COUT == 32) {
+    // the tensor-core kernel streams rows with TMA (16-B row strides: W % 4 == 0)
+    if (g_train_conv_impl == 0 && W % 4 == 0) return wgrad_tc32(x, dout, B, H, W, dw, db, g_wgrad_parts, st);
     const size_t smem = sizeof(float) * ((size_t)32 * (W32_TY + 2) * (W32_TX + 2) + W32_TY * W32_TX * W32_PAD);
     static bool attr32 = false;
     if (!attr32) {
@@ -452,9 +458,13 @@ int ht_train_act_bytes(int channels, int blocks, int B, int H, int W, int64_t *b
   return HT_OK;
 }
 
-int ht_policy_forward_train(const void *packed, int C, int NB, const float *x, int B, int H,
-                            int W, void *act, float *p, void *stream) {
+// Training forward + sigmoid; non-finite logits OR'ed into *flag_dev (device
+// int) without waiting for the GPU: the caller checks the flag later, e.g.
+// once per training step before the parameter update.
+int ht_policy_forward_train_async(const void *packed, int C, int NB, const float *x, int B, int H, int W,
+                                  void *act, float *p, int *flag_dev, void *stream) {
   HT_REQUIRE(B > 0 && H > 0 && W > 0, "input must be non-empty (B=%d H=%d W=%d)", B, H, W);
+  HT_REQUIRE(flag_dev != nullptr, "flag_dev must be a device int");
   ht::reset_launches();
   cudaStream_t st = (cudaStream_t)stream;
   const size_t a = (size_t)B * C * H * W;
@@ -463,13 +473,24 @@ int ht_policy_forward_train(const void *packed, int C, int NB, const float *x, i
   int rc = ht::simt_forward(packed, C, NB, x, B, H, W, scratch, true, logits, st);
   if (rc) return rc;
   // sigmoid + finite check (nn.py:147-149)
+  const int64_t n = (int64_t)B * H * W;
+  ht::sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(logits, p, n, flag_dev);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+int ht_policy_forward_train(const void *packed, int C, int NB, const float *x, int B, int H,
+                            int W, void *act, float *p, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
   int *d_flag;
   HT_CUDA(cudaMallocAsync(&d_flag, sizeof(int), st));
   HT_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
-  const int64_t n = (int64_t)B * H * W;
-  ht::sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(logits, p, n, d_flag);
-  ht::count_launch();
-  HT_CHECK_LAUNCH();
+  const int rc = ht_policy_forward_train_async(packed, C, NB, x, B, H, W, act, p, d_flag, stream);
+  if (rc) {
+    cudaFreeAsync(d_flag, st);
+    return rc;
+  }
   int hflag = 0;
   HT_CUDA(cudaMemcpyAsync(&hflag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   HT_CUDA(cudaFreeAsync(d_flag, st));
@@ -542,6 +563,23 @@ int ht_conv3x3_32(const float *x, int B, int H, int W, const float *w, const flo
   ht::g_train_conv_impl = impl;
   const int rc = ht::conv_fwd<32, 32>(x, B, H, W, w, bias, mask, resid, out, relu, (cudaStream_t)stream);
   ht::g_train_conv_impl = keep;
+  return rc;
+}
+
+// Weight / bias gradient of one 3x3 convolution 32 -> 32: dw (32,32,3,3) and
+// db (32) fp64 accumulate (+=); impl 0 = tcgen05 with `parts` (2 or 3) bf16
+// parts, 1 = fp32 SIMT.  For tests.
+int ht_wgrad3x3_32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int impl,
+                   int parts, void *stream) {
+  HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty input");
+  HT_REQUIRE(impl == 0 || impl == 1, "impl must be 0 (tensor core) or 1 (simt)");
+  HT_REQUIRE(parts == 2 || parts == 3, "parts must be 2 or 3");
+  const int keep = ht::g_train_conv_impl, keep_parts = ht::g_wgrad_parts;
+  ht::g_train_conv_impl = impl;
+  ht::g_wgrad_parts = parts;
+  const int rc = ht::conv_wgrad<32, 32>(x, dout, B, H, W, dw, db, (cudaStream_t)stream);
+  ht::g_train_conv_impl = keep;
+  ht::g_wgrad_parts = keep_parts;
   return rc;
 }
 

@@ -180,9 +180,12 @@ class PolicyNetwork:
         p = self.forward_device(xd)
         return p.double().cpu().numpy()[:, None]
 
-    def forward_device(self, x):
+    def forward_device(self, x, flag=None):
         """Training forward on a device tensor x (B, 2, H, W) float32 ->
-        p (B, H, W) float32 device tensor; activations cached."""
+        p (B, H, W) float32 device tensor; activations cached.  Raises
+        FloatingPointError on non-finite logits (nn.py:147-148) -- or, with
+        flag (an int32 device tensor), ORs that condition into flag[0]
+        without waiting for the GPU, for the caller to check later."""
         torch = _torch()
         _lib.require_cuda()
         self.sync()
@@ -196,8 +199,12 @@ class PolicyNetwork:
         act = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
         p = torch.empty((B, H, W), dtype=torch.float32, device=x.device)
         self._cache = None
-        _lib.call("ht_policy_forward_train", _lib.ptr(self._packed), self.channels, self.blocks,
-                  _lib.ptr(x), B, H, W, _lib.ptr(act), _lib.ptr(p), _lib.stream_ptr())
+        if flag is None:
+            _lib.call("ht_policy_forward_train", _lib.ptr(self._packed), self.channels, self.blocks,
+                      _lib.ptr(x), B, H, W, _lib.ptr(act), _lib.ptr(p), _lib.stream_ptr())
+        else:
+            _lib.call("ht_policy_forward_train_async", _lib.ptr(self._packed), self.channels, self.blocks,
+                      _lib.ptr(x), B, H, W, _lib.ptr(act), _lib.ptr(p), _lib.ptr(flag), _lib.stream_ptr())
         self._cache = (x, act, p, B, H, W)
         return p
 

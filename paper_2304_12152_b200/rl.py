@@ -276,11 +276,18 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     lo, hi = shard_range(bs, rank, world)
     crops, noises = draw_batch(dataset, cfg, rng, device=dev, keep=range(lo, hi))
     grad = torch.zeros(net.num_params(), dtype=torch.float64, device=dev)
-    stats = torch.zeros(3, dtype=torch.float64, device=dev)  # reward, bin_gap, l_as sums
+    # reward, bin_gap, l_as sums, non-finite flag of the two forwards (one
+    # all-reduce, one read-back per step)
+    stats = torch.zeros(4, dtype=torch.float64, device=dev)
+    nonfinite = torch.zeros(2, dtype=torch.int32, device=dev)
+    # RNG states at the two forwards: a non-finite logit is detected once per
+    # step (no wait per forward) and raised with the stream where the
+    # reference's forward (nn.py:147-148) would have raised
+    rng_at_fwd = [rng.state_words(), None]
     p = None
     if hi > lo:
-        cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).to(dev)
-        p = net.forward_device(torch.stack((cd, noises), dim=1))
+        cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory().to(dev, non_blocking=True)
+        p = net.forward_device(torch.stack((cd, noises), dim=1), flag=nonfinite[0:1])
     # action uniforms for every sample, in order (rl.py:249 -> rl.py:68): this
     # rank's shard is one contiguous stretch of the stream, drawn on the GPU
     # in one launch; the other ranks' stretches are skipped (jump-ahead)
@@ -327,17 +334,25 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
             if glo <= i < ghi:
                 starts.append(rng.state_words())
             rng.jump(draws)
+        rng_at_fwd[1] = rng.state_words()
         if ghi > glo:
             znoise = gaussian_maps_device(starts, size, size, device=dev)
-            gd = torch.tensor([grays[i] for i in range(glo, ghi)], dtype=torch.float64)
-            gd = gd.to(torch.float32).to(dev)[:, None, None].expand(-1, size, size)
-            pg = net.forward_device(torch.stack((gd, znoise), dim=1).contiguous())
+            gd = torch.tensor([grays[i] for i in range(glo, ghi)], dtype=torch.float32)
+            gd = gd.pin_memory().to(dev, non_blocking=True)[:, None, None].expand(-1, size, size)
+            pg = net.forward_device(torch.stack((gd, znoise), dim=1).contiguous(), flag=nonfinite[1:2])
             part = _part_cache(size)
             loss, dpg = anisotropy_device(pg, part, scale=cfg.w_a / ba)
             net.backward_device(dpg, grad)
             stats[2] += loss.sum()
+    stats[3] = nonfinite[0].double() + 2.0 * nonfinite[1].double()
     allreduce_sum_(grad, stats, group=group)   # the step's one exchange
     st = stats.cpu().numpy()
+    if st[3] != 0.0:
+        # first forward with a non-finite logit on any rank; parameters and
+        # Adam state untouched, RNG as the reference leaves it when it raises
+        which = 0 if int(st[3]) % 2 == 1 else 1
+        rng.set_state_words(rng_at_fwd[which])
+        raise FloatingPointError("non-finite logits")
     mean_reward = float(st[0] / bs)
     bin_gap = float(st[1] / (bs * size * size))
     l_as = float(st[2] / (cfg.anisotropy_batch_size or bs)) if run_aniso else math.nan

@@ -168,3 +168,31 @@ def test_train_step_vs_reference(tag, ch, nb, bs, crop, ba):
     dn = np.array([np.linalg.norm(a) for a in np.split(p1 - p0, np.cumsum(
         [q.value.size for q in net.params()])[:-1])])
     assert np.all(np.abs(dn / g[f"{tag}_dparam_norms"] - 1) < 1e-3)
+
+
+def test_train_step_nonfinite_raises_before_update():
+    """A non-finite logit (nn.py:147-148) raises FloatingPointError from
+    train_step with the parameters, the Adam state and the RNG stream where
+    the reference leaves them (its forward raises before backward / Adam).
+    The device forward only flags it; train_step checks once per step."""
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    g = golden("train.npz")
+    cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
+                         anisotropy_batch_size=2, hvs_model="gaussian")
+    ds = list(g["mini_ds"])
+    net = PolicyNetwork(8, 2)
+    adam = Adam(net.params())
+    rng = Rng(cfg.seed)
+    net.init_params(rng)
+    net.conv_out.bias.value[0] = np.inf          # every logit non-finite
+    expect = Rng(0)
+    expect.set_state_words(rng.state_words())
+    rl.draw_batch(ds, cfg, expect)               # the reference raises right after this
+    p0 = net.flat_values()
+    with pytest.raises(FloatingPointError):
+        rl.train_step(net, adam, ds, cfg, rng, 0)
+    assert np.array_equal(net.flat_values(), p0, equal_nan=True)
+    assert adam.t == 0
+    assert rng.state_words() == expect.state_words()
