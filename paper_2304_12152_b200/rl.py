@@ -130,6 +130,52 @@ def make_sample(p, c, z, rng, cfg=None, level_count=2):
                          ceil_vals=ceil_vals, p_ceil=p_ceil, level_count=level_count, ctx=ctx)
 
 
+def exact_gradient_oracle(p, c, cfg=None, region="full", level_count=2):
+    """rl.py:139-164: d E[R] / d p by enumerating every joint action map
+    (each pixel at the lower or upper point of its two-point cast), at most 20
+    pixels.  The 2^n rewards are evaluated on the GPU in batched launches of
+    the reward kernel (maps passed as given action maps); the weighting is
+    host arithmetic.  For L > 2, p is the value map and upper-level mass moves
+    at (L - 1) per unit value."""
+    torch = _torch()
+    _lib.require_cuda()
+    p = np.asarray(p, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    n = p.size
+    if n > 20:
+        raise ValueError("oracle enumeration limited to 20 pixels")
+    if c.shape != p.shape:
+        raise ValueError("p and c must have the same shape")
+    if region != "full":
+        if region == "valid":
+            raise NotImplementedError("region='valid' is an evaluation metric outside the GPU hot "
+                                      "path (use region='full')")
+        raise ValueError(f"unknown region {region!r}")
+    cfg = cfg or MetricConfig()
+    floor_vals, ceil_vals, p_ceil = _cast_two_point(p, level_count)
+    fv, cv, q = floor_vals.ravel(), ceil_vals.ravel(), p_ceil.ravel()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    total = 1 << n
+    grad = np.zeros(n)
+    chunk = 1 << 16
+    cd = None
+    for b0 in range(0, total, chunk):
+        b1 = min(total, b0 + chunk)
+        up = ((np.arange(b0, b1)[:, None] >> np.arange(n)[None, :]) & 1).astype(bool)
+        m = np.where(up, cv[None], fv[None]).reshape((b1 - b0,) + p.shape)
+        if cd is None or cd.shape[0] != b1 - b0:
+            cd = torch.from_numpy(np.broadcast_to(c, m.shape).astype(np.float32).copy()).to(dev)
+        md = torch.from_numpy(m.astype(np.float32)).to(dev)
+        _, _, rew = reward_signal_device(md, None, cd, cfg, want_signal=False, levels=level_count)
+        r = rew.cpu().numpy()
+        prob_each = np.where(up, q[None], 1.0 - q[None])
+        sign = np.where(up, 1.0, -1.0)
+        for a in range(n):
+            rest = np.prod(np.delete(prob_each, a, axis=1), axis=1)
+            grad[a] += float(np.sum(r * sign[:, a] * rest))
+    return (grad * (level_count - 1)).reshape(p.shape)
+
+
 def _two_point_diff(sample):
     """rl.py:96-103: R(upper) - R(lower) per pixel (0 where collapsed)."""
     from .metrics import delta_map
