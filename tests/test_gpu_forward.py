@@ -192,3 +192,31 @@ def test_engine_draws_noise_on_device_in_infer_halftone_order():
     assert torch.equal(o1, o2)
     assert rng.state_words() == zr.state_words()
     assert eng.h2d_bytes(device_noise=True) * 2 == eng.h2d_bytes()
+
+
+def test_zero_second_convs_make_blocks_identity_bitwise():
+    """Reference property (test_nn.py `test_zero_second_conv_is_identity`):
+    a residual block whose second conv is zero is the identity.  So a
+    16-block network with every conv2 zeroed must give, bit for bit, the
+    0-block network with the same conv_in / conv_out -- through every pass of
+    the fused kernel (fp32 residual stream carried exactly), at 8 x 512^2."""
+    import torch
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = _net(0.05)
+    for blk in net.res:
+        blk.conv2.weight.value[...] = 0.0
+        blk.conv2.bias.value[...] = 0.0
+    net0 = PolicyNetwork(32, 0)
+    for a, b in ((net0.conv_in, net.conv_in), (net0.conv_out, net.conv_out)):
+        a.weight.value[...] = b.weight.value
+        a.bias.value[...] = b.bias.value
+    B, H, W = 8, 512, 512
+    c = torch.from_numpy(np.stack([synth.contone(H, W, seed=70 + i) for i in range(B)]).astype(np.float32)).cuda()
+    z = torch.from_numpy(np.stack([gaussian_noise_map_f32(Rng(80 + i), W, H) for i in range(B)])).cuda()
+    p16 = torch.empty((B, H, W), dtype=torch.float32, device="cuda")
+    p0 = torch.empty_like(p16)
+    net.halftone_device(c, z, p_out=p16)
+    net0.halftone_device(c, z, p_out=p0)
+    assert torch.equal(p16, p0)
