@@ -449,12 +449,15 @@ def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None):
 class HalftoneEngine:
     """Reusable batched halftoner for a fixed (B, H, W): host contone/noise
     (float32, ideally pinned) in, uint8 halftones (1 = white) or PBM P4
-    payloads out.  The batch is split into `chunks` groups of images that
-    flow through H2D -> fused K1 kernel -> D2H on alternating CUDA streams, so
-    copies of one chunk overlap the kernel of another.  Every call performs
-    the full host->device->host round trip."""
+    payloads out.  A call (or submit) performs the full host->device->host
+    round trip of one batch.  Within a batch, `chunks` groups of images flow
+    through H2D -> fused K1 kernel -> D2H on alternating CUDA streams, so
+    copies of one chunk overlap the kernel of another (lowest latency for a
+    single call).  For throughput, submit()/wait() stream batches through
+    `depth` sets of device buffers: batch i+1's copies overlap batch i's
+    kernels, and one chunk per batch keeps the launches few."""
 
-    def __init__(self, net, B, H, W, chunks=4, output="h", impl=None):
+    def __init__(self, net, B, H, W, chunks=4, output="h", impl=None, depth=2):
         torch = _torch()
         _lib.require_cuda()
         if output not in ("h", "pbm", "p"):
@@ -471,19 +474,29 @@ class HalftoneEngine:
         self.groups = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
         dev = net.device
         self.dev = dev
-        # forward/copy streams at high priority: the block scheduler then
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        # `depth` sets of device buffers + streams: submitted batches rotate
+        # through them, so batch i+1's copies and kernels run beside batch i's
+        # (a set is reused, in its streams' order, by batch i+depth).  The
+        # forward/copy streams run at high priority: the block scheduler then
         # prefers the fused kernel's CTAs over the side stream's noise blocks
-        self.streams = [torch.cuda.Stream(dev, priority=-1) for _ in range(2)]
-        self.noise_stream = torch.cuda.Stream(dev, priority=0)
-        self.c = torch.empty((B, H, W), dtype=torch.float32, device=dev)
-        self.z = torch.empty((B, H, W), dtype=torch.float32, device=dev)
-        if output == "pbm":
-            self.out = torch.empty((B, H, (W + 7) // 8), dtype=torch.uint8, device=dev)
-        elif output == "h":
-            self.out = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
-        else:
-            self.out = torch.empty((B, H, W), dtype=torch.float32, device=dev)
-        self.ws = [None, None]
+        self._sets = []
+        for _ in range(depth):
+            if output == "pbm":
+                out = torch.empty((B, H, (W + 7) // 8), dtype=torch.uint8, device=dev)
+            elif output == "h":
+                out = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+            else:
+                out = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+            self._sets.append({
+                "streams": [torch.cuda.Stream(dev, priority=-1) for _ in range(2)],
+                "noise": torch.cuda.Stream(dev, priority=0),
+                "c": torch.empty((B, H, W), dtype=torch.float32, device=dev),
+                "z": torch.empty((B, H, W), dtype=torch.float32, device=dev),
+                "out": out, "ws": [None, None]})
+        self._next = 0
+        self.out = self._sets[0]["out"]
         net.sync()
 
     def out_shape(self):
@@ -500,10 +513,24 @@ class HalftoneEngine:
         z_host: the (B,H,W) float32 noise as a CPU tensor, or an Rng -- then
         image i's noise map is gaussian_noise_map(rng, W, H) drawn on the GPU
         in image order, as B calls of rl.infer_halftone would draw it
-        (rl.py:306-311); out_host: CPU tensor shaped out_shape()."""
+        (rl.py:306-311); out_host: CPU tensor shaped out_shape().  Returns
+        out_host once it holds the result."""
+        self.wait(self.submit(c_host, z_host, out_host))
+        return out_host
+
+    def submit(self, c_host, z_host, out_host):
+        """Enqueue one batch (H2D -> fused forward -> D2H) without waiting and
+        return a ticket for wait().  Back-to-back submits pipeline: the next
+        batch's first copies and kernel overlap this batch's tail (the device
+        buffers are reused in stream order).  c_host / z_host must stay
+        unchanged and out_host unread until the ticket is waited on; give
+        batches in flight distinct out_host buffers."""
         torch = _torch()
         cur = torch.cuda.current_stream(self.dev)
         device_noise = isinstance(z_host, Rng)
+        st = self._sets[self._next % len(self._sets)]
+        self._next += 1
+        streams, zbuf, cbuf, obuf, ws = st["streams"], st["z"], st["c"], st["out"], st["ws"]
         ready = [None] * len(self.groups)
         if device_noise:
             # every chunk's noise maps, drawn in image order from the stream;
@@ -512,35 +539,48 @@ class HalftoneEngine:
             # pipe and 1/8 of the register file free)
             n = self.H * self.W
             for k, (a, b) in enumerate(self.groups):
-                ns = self.streams[0] if k == 0 else self.noise_stream
+                ns = streams[0] if k == 0 else st["noise"]
                 ns.wait_stream(cur)
+                # the previous batch on this buffer set read this chunk's z
+                ns.wait_stream(streams[k % 2])
                 with torch.cuda.stream(ns):
                     if n % 2 == 0:     # maps of even size are back-to-back in the stream
-                        z_host.gaussians_device((b - a) * n, out=self.z[a:b].view(-1))
+                        z_host.gaussians_device((b - a) * n, out=zbuf[a:b].view(-1))
                     else:              # odd size: each map burns one draw
                         for i in range(a, b):
-                            z_host.gaussians_device(n, out=self.z[i].view(-1))
+                            z_host.gaussians_device(n, out=zbuf[i].view(-1))
                     ready[k] = torch.cuda.Event()
                     ready[k].record(ns)
         for k, (a, b) in enumerate(self.groups):
-            s = self.streams[k % 2]
+            s = streams[k % 2]
             s.wait_stream(cur)
             with torch.cuda.stream(s):
-                self.c[a:b].copy_(c_host[a:b], non_blocking=True)
+                cbuf[a:b].copy_(c_host[a:b], non_blocking=True)
                 if device_noise:
                     s.wait_event(ready[k])
                 else:
-                    self.z[a:b].copy_(z_host[a:b], non_blocking=True)
+                    zbuf[a:b].copy_(z_host[a:b], non_blocking=True)
                 kw = {"h_out" if self.output == "h" else
-                      ("pbm_out" if self.output == "pbm" else "p_out"): self.out[a:b]}
-                self.ws[k % 2] = self.net.halftone_device(
-                    self.c[a:b], self.z[a:b], impl=self.impl, workspace=self.ws[k % 2],
+                      ("pbm_out" if self.output == "pbm" else "p_out"): obuf[a:b]}
+                ws[k % 2] = self.net.halftone_device(
+                    cbuf[a:b], zbuf[a:b], impl=self.impl, workspace=ws[k % 2],
                     stream=s, **kw)
-                out_host[a:b].copy_(self.out[a:b], non_blocking=True)
-        for s in self.streams + [self.noise_stream]:
-            cur.wait_stream(s)
-        cur.synchronize()
-        return out_host
+                out_host[a:b].copy_(obuf[a:b], non_blocking=True)
+        ticket = []
+        for s in streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            ticket.append(e)
+        return ticket
+
+    def wait(self, ticket):
+        """Block until a submitted batch's result is in its out_host; later
+        work on the current stream is ordered after it."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.dev)
+        for e in ticket:
+            cur.wait_event(e)
+            e.synchronize()
 
 
 def halftone_batch(net, contones, noises, output="h", chunks=4):

@@ -220,3 +220,34 @@ def test_zero_second_convs_make_blocks_identity_bitwise():
     net.halftone_device(c, z, p_out=p16)
     net0.halftone_device(c, z, p_out=p0)
     assert torch.equal(p16, p0)
+
+
+@pytest.mark.parametrize("noise", ["host", "device"])
+def test_engine_streamed_batches_equal_sequential_calls(noise):
+    """HalftoneEngine.submit/wait with batches in flight (device buffers
+    reused in stream order) gives exactly the per-call results; with device
+    noise the RNG stream is consumed batch after batch as sequential calls
+    would."""
+    import torch
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    net = _net(0.05)
+    B, H, W, n = 5, 33, 70, 4
+    r = Rng(3)
+    cs = [torch.from_numpy(r.uniforms(B * H * W).reshape(B, H, W).astype(np.float32)).pin_memory()
+          for _ in range(n)]
+    zs = [torch.from_numpy(r.gaussians_f32(B * H * W).reshape(B, H, W)).pin_memory() for _ in range(n)]
+    eng = rl.HalftoneEngine(net, B, H, W, chunks=3, output="h")
+    seq, rs = [], Rng(11)
+    for i in range(n):
+        o = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+        seq.append(eng(cs[i], zs[i] if noise == "host" else rs, o).clone())
+    outs = [torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory() for _ in range(n)]
+    rs2 = Rng(11)
+    tickets = [eng.submit(cs[i], zs[i] if noise == "host" else rs2, outs[i]) for i in range(n)]
+    for t in tickets:
+        eng.wait(t)
+    for i in range(n):
+        assert torch.equal(outs[i], seq[i]), i
+    if noise == "device":
+        assert rs2.state_words() == rs.state_words()
