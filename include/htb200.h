@@ -166,10 +166,10 @@ int ht_train_act_bytes(int channels, int blocks, int B, int H, int W,
 int ht_policy_forward_train(const void *packed_dev, int channels, int blocks,
                             const float *x_dev, int B, int H, int W,
                             void *act_dev, float *p_dev, void *stream);
-/* Same without waiting for the GPU: non-finite logits are OR'ed into
- * *flag_dev (a device int the caller zeroes and checks later -- rl.train_step
- * checks it once per step, before the parameter update, and raises as
- * nn.py:147-148 would). */
+/* Same without waiting for the GPU: sample b's non-finite logits are OR'ed
+ * into flag_dev[b] (B device ints the caller zeroes and checks later --
+ * rl.train_step checks them once per step, before the parameter update, and
+ * raises as nn.py:147-148 would). */
 int ht_policy_forward_train_async(const void *packed_dev, int channels, int blocks,
                                   const float *x_dev, int B, int H, int W,
                                   void *act_dev, float *p_dev, int *flag_dev, void *stream);

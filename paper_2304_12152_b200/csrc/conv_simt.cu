@@ -9,6 +9,8 @@
 // params() order.
 #include <math.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ht {
@@ -172,12 +174,14 @@ conv3x3_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dout
 
 // ---------------------------------------------------------------------------
 // elementwise helpers
+// p = sigmoid(logit); a non-finite logit of sample i / per_flag sets
+// nonfinite[i / per_flag]
 __global__ void sigmoid_kernel(const float *__restrict__ logit, float *__restrict__ p,
-                               int64_t n, int *__restrict__ nonfinite) {
+                               int64_t n, int *__restrict__ nonfinite, int64_t per_flag) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float l = logit[i];
-  if (!isfinite(l)) atomicOr(nonfinite, 1);
+  if (!isfinite(l)) atomicOr(nonfinite + i / per_flag, 1);
   p[i] = 1.f / (1.f + expf(-l));
 }
 
@@ -458,9 +462,9 @@ int ht_train_act_bytes(int channels, int blocks, int B, int H, int W, int64_t *b
   return HT_OK;
 }
 
-// Training forward + sigmoid; non-finite logits OR'ed into *flag_dev (device
-// int) without waiting for the GPU: the caller checks the flag later, e.g.
-// once per training step before the parameter update.
+// Training forward + sigmoid; sample b's non-finite logits OR'ed into
+// flag_dev[b] (B device ints) without waiting for the GPU: the caller checks
+// the flags later, e.g. once per training step before the parameter update.
 int ht_policy_forward_train_async(const void *packed, int C, int NB, const float *x, int B, int H, int W,
                                   void *act, float *p, int *flag_dev, void *stream) {
   HT_REQUIRE(B > 0 && H > 0 && W > 0, "input must be non-empty (B=%d H=%d W=%d)", B, H, W);
@@ -474,7 +478,8 @@ int ht_policy_forward_train_async(const void *packed, int C, int NB, const float
   if (rc) return rc;
   // sigmoid + finite check (nn.py:147-149)
   const int64_t n = (int64_t)B * H * W;
-  ht::sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(logits, p, n, flag_dev);
+  ht::sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(logits, p, n, flag_dev,
+                                                                   (int64_t)H * W);
   ht::count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
@@ -482,20 +487,22 @@ int ht_policy_forward_train_async(const void *packed, int C, int NB, const float
 
 int ht_policy_forward_train(const void *packed, int C, int NB, const float *x, int B, int H,
                             int W, void *act, float *p, void *stream) {
+  HT_REQUIRE(B > 0 && H > 0 && W > 0, "input must be non-empty (B=%d H=%d W=%d)", B, H, W);
   cudaStream_t st = (cudaStream_t)stream;
   int *d_flag;
-  HT_CUDA(cudaMallocAsync(&d_flag, sizeof(int), st));
-  HT_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  HT_CUDA(cudaMallocAsync(&d_flag, sizeof(int) * B, st));
+  HT_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int) * B, st));
   const int rc = ht_policy_forward_train_async(packed, C, NB, x, B, H, W, act, p, d_flag, stream);
   if (rc) {
     cudaFreeAsync(d_flag, st);
     return rc;
   }
-  int hflag = 0;
-  HT_CUDA(cudaMemcpyAsync(&hflag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  std::vector<int> hflag(B, 0);
+  HT_CUDA(cudaMemcpyAsync(hflag.data(), d_flag, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
   HT_CUDA(cudaFreeAsync(d_flag, st));
   HT_CUDA(cudaStreamSynchronize(st));
-  if (hflag) return ht::fail(HT_E_NONFINITE, "non-finite logits");
+  for (int b = 0; b < B; ++b)
+    if (hflag[b]) return ht::fail(HT_E_NONFINITE, "non-finite logits");
   return HT_OK;
 }
 

@@ -184,8 +184,9 @@ class PolicyNetwork:
         """Training forward on a device tensor x (B, 2, H, W) float32 ->
         p (B, H, W) float32 device tensor; activations cached.  Raises
         FloatingPointError on non-finite logits (nn.py:147-148) -- or, with
-        flag (an int32 device tensor), ORs that condition into flag[0]
-        without waiting for the GPU, for the caller to check later."""
+        flag (an int32 device tensor of B entries), ORs sample b's condition
+        into flag[b] without waiting for the GPU, for the caller to check
+        later."""
         torch = _torch()
         _lib.require_cuda()
         self.sync()

@@ -322,52 +322,27 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     lo, hi = shard_range(bs, rank, world)
     crops, noises = draw_batch(dataset, cfg, rng, device=dev, keep=range(lo, hi))
     grad = torch.zeros(net.num_params(), dtype=torch.float64, device=dev)
-    # reward, bin_gap, l_as sums, non-finite flag of the two forwards (one
-    # all-reduce, one read-back per step)
+    # reward, bin_gap, l_as sums, non-finite flags (one all-reduce, one
+    # read-back per step)
     stats = torch.zeros(4, dtype=torch.float64, device=dev)
-    nonfinite = torch.zeros(2, dtype=torch.int32, device=dev)
-    # RNG states at the two forwards: a non-finite logit is detected once per
-    # step (no wait per forward) and raised with the stream where the
-    # reference's forward (nn.py:147-148) would have raised
+    # RNG states at the reference's two forwards: a non-finite logit is
+    # detected once per step (no wait per forward) and raised with the
+    # stream where the reference's forward (nn.py:147-148) would have raised
     rng_at_fwd = [rng.state_words(), None]
-    p = None
-    if hi > lo:
-        cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory().to(dev, non_blocking=True)
-        p = net.forward_device(torch.stack((cd, noises), dim=1), flag=nonfinite[0:1])
     # action uniforms for every sample, in order (rl.py:249 -> rl.py:68): this
     # rank's shard is one contiguous stretch of the stream, drawn on the GPU
-    # in one launch; the other ranks' stretches are skipped (jump-ahead)
+    # in one launch; the other ranks' stretches are skipped (jump-ahead).  No
+    # draw depends on the forward, so all of the step's draws come first.
     n = size * size
     rng.jump(lo * n)
     ud = rng.uniforms_device((hi - lo) * n, device=dev).view(hi - lo, size, size) if hi > lo else None
     rng.jump((bs - hi) * n)
-    reinforce = cfg.estimator in ("reinforce", "reinforce_meanbaseline")
-    if hi > lo:
-        if not reinforce:
-            m, sig, rew = reward_signal_device(p, ud, cd, mcfg, scale=1.0 / bs, levels=cfg.levels,
-                                               estimator=cfg.estimator)
-        else:
-            m, _, rew = reward_signal_device(p, ud, cd, mcfg, want_signal=False)
-    if cfg.estimator == "reinforce_meanbaseline":
-        # baseline = mean reward of the GLOBAL batch: one extra scalar
-        # all-reduce, joined by every rank (also those without samples)
-        rsum = rew.sum().reshape(1) if hi > lo else torch.zeros(1, dtype=torch.float64, device=dev)
-        allreduce_sum_(rsum, group=group)
-        baseline = float(rsum.item()) / bs
-    else:
-        baseline = 0.0
-    if hi > lo:
-        if reinforce:
-            sig = reinforce_signal_device(p, m, rew, baseline, scale=1.0 / bs)
-        if signal_override is not None:
-            mh = m.double().cpu().numpy()
-            sig = torch.from_numpy(np.stack([signal_override(lo + i, mh[i]) / bs
-                                             for i in range(hi - lo)]).astype(np.float32)).to(dev)
-        net.backward_device(sig, grad)
-        stats[0] += rew.sum()
-        _lib.call("ht_bin_gap_sum", _lib.ptr(p), p.numel(), _lib.ptr(stats[1:2]),
-                  _lib.stream_ptr())
     run_aniso = cfg.w_a != 0.0 and (cfg.levels == 2 or cfg.multitone_anisotropy)
+    nm, ng = hi - lo, 0
+    inputs = []
+    if nm:
+        cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory().to(dev, non_blocking=True)
+        inputs.append(torch.stack((cd, noises), dim=1))
     if run_aniso:
         ba = cfg.anisotropy_batch_size or bs
         grays = [rng.uniform() for _ in range(ba)]
@@ -381,16 +356,56 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
                 starts.append(rng.state_words())
             rng.jump(draws)
         rng_at_fwd[1] = rng.state_words()
-        if ghi > glo:
+        ng = ghi - glo
+        if ng:
             znoise = gaussian_maps_device(starts, size, size, device=dev)
             gd = torch.tensor([grays[i] for i in range(glo, ghi)], dtype=torch.float32)
             gd = gd.pin_memory().to(dev, non_blocking=True)[:, None, None].expand(-1, size, size)
-            pg = net.forward_device(torch.stack((gd, znoise), dim=1).contiguous(), flag=nonfinite[1:2])
-            part = _part_cache(size)
-            loss, dpg = anisotropy_device(pg, part, scale=cfg.w_a / ba)
-            net.backward_device(dpg, grad)
-            stats[2] += loss.sum()
-    stats[3] = nonfinite[0].double() + 2.0 * nonfinite[1].double()
+            inputs.append(torch.stack((gd, znoise), dim=1))
+    # one forward + one backward over this rank's MARL crops and gray images
+    # (the reference's two forwards, batched: samples are independent and the
+    # parameters do not change in between); sample b's non-finite flag
+    nonfinite = torch.zeros(max(nm + ng, 1), dtype=torch.int32, device=dev)
+    if nm + ng:
+        x = inputs[0] if len(inputs) == 1 else torch.cat(inputs)
+        p_all = net.forward_device(x.contiguous(), flag=nonfinite)
+    dps = []
+    reinforce = cfg.estimator in ("reinforce", "reinforce_meanbaseline")
+    if nm:
+        p = p_all[:nm]
+        if not reinforce:
+            m, sig, rew = reward_signal_device(p, ud, cd, mcfg, scale=1.0 / bs, levels=cfg.levels,
+                                               estimator=cfg.estimator)
+        else:
+            m, _, rew = reward_signal_device(p, ud, cd, mcfg, want_signal=False)
+    if cfg.estimator == "reinforce_meanbaseline":
+        # baseline = mean reward of the GLOBAL batch: one extra scalar
+        # all-reduce, joined by every rank (also those without samples)
+        rsum = rew.sum().reshape(1) if nm else torch.zeros(1, dtype=torch.float64, device=dev)
+        allreduce_sum_(rsum, group=group)
+        baseline = float(rsum.item()) / bs
+    else:
+        baseline = 0.0
+    if nm:
+        if reinforce:
+            sig = reinforce_signal_device(p, m, rew, baseline, scale=1.0 / bs)
+        if signal_override is not None:
+            mh = m.double().cpu().numpy()
+            sig = torch.from_numpy(np.stack([signal_override(lo + i, mh[i]) / bs
+                                             for i in range(nm)]).astype(np.float32)).to(dev)
+        dps.append(sig)
+        stats[0] += rew.sum()
+        _lib.call("ht_bin_gap_sum", _lib.ptr(p), p.numel(), _lib.ptr(stats[1:2]),
+                  _lib.stream_ptr())
+    if ng:
+        part = _part_cache(size)
+        loss, dpg = anisotropy_device(p_all[nm:], part, scale=cfg.w_a / ba)
+        dps.append(dpg)
+        stats[2] += loss.sum()
+    if dps:
+        net.backward_device(dps[0] if len(dps) == 1 else torch.cat(dps), grad)
+    stats[3] = (nonfinite[:nm].amax().double() if nm else 0.0) + \
+        2.0 * (nonfinite[nm:nm + ng].amax().double() if ng else 0.0)
     allreduce_sum_(grad, stats, group=group)   # the step's one exchange
     st = stats.cpu().numpy()
     if st[3] != 0.0:
