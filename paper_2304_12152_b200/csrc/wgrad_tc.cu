@@ -26,8 +26,12 @@
 //   32 channels x 32 px, 128-B swizzled; dout: 2 rows x 32 channels x 44 px,
 //   176-B rows) into an NR-slot ring -- out-of-image pixels arrive
 //   as zeros, no load instructions or bounds checks in the converters;
-// * 16 converter warps turn a raw slot into split-bf16 UMMA core matrices
-//   (conflict-free shared reads and writes) in one of two operand buffers;
+// * 16 converter warps split a raw slot into bf16 parts: 8 warps write the
+//   x rows straight into the MMA's A operand in TMEM (TMEM lane quarter = x
+//   row, lane = channel, bf16 pairs of 16 pixels per warp), 8 warps the
+//   shifted dout copies as UMMA core matrices in shared memory (two
+//   buffers); keeping A out of shared memory cuts the operand traffic of a
+//   pipe the converters and the MMAs share;
 // * one warp issues the MMAs in tile order;
 // * the tensor core adds into its fp32 accumulator with an error that grows
 //   with the chain length (1.2e-5 with one chain per CTA over 8 x 256^2), so
@@ -54,9 +58,8 @@ constexpr int CGB = (WT / 8) * 128;   // one 8-channel group of a row: WT/8 core
 constexpr int ROWB = 4 * CGB;         // 32 channels of a row, one part
 constexpr int NCOL = 2 * 3 * C;       // 192 accumulator columns (s, kx, co)
 constexpr int NCONV = 512;            // converter threads
-constexpr int X_UNITS = XR * C * (WT / 8);   // (x row, channel, 8-pixel chunk): one per converter
 constexpr int D_UNITS = TY * C * (WT / 8);   // (dout row, channel, 8-pixel chunk)
-static_assert(X_UNITS == NCONV && D_UNITS <= NCONV, "one x unit per converter thread");
+static_assert(XR * C == 128 && D_UNITS == NCONV - 256, "x rows on warps 0-3 / 12-15, dout units on 4-11");
 // dout box: pixels x0-4 .. x0+39 (the innermost box start must be 16-B
 // aligned; 176-B rows keep 8 consecutive channels on distinct bank groups)
 constexpr int DBOX = 44;
@@ -66,18 +69,19 @@ constexpr int RAW_SLOT = (RAW_X + RAW_D + 1023) / 1024 * 1024;
 constexpr int NB = 2;                 // operand buffers
 constexpr uint32_t IDESC =
     (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-constexpr int D_COL = 0, D2_COL = 256;   // TMEM: chain accumulator, running sum
+// TMEM: chain accumulator D (192 columns), the x operand A (NB buffers x NP
+// parts x 16 columns: 32 pixels of bf16 pairs per lane), running sum D2
+constexpr int D_COL = 0, A_COL = 192, D2_COL = 288;
 
 template <int NP>
 struct Lay {
   static constexpr int NPROD = NP == 2 ? 3 : 6;
   static constexpr int F = NP == 2 ? 16 : 8;        // tiles per accumulation chain (96 MMAs)
-  static constexpr int NR = NP == 2 ? 4 : 3;        // raw ring slots
-  static constexpr int X_PART = XR * ROWB;
+  static constexpr int NR = 4;                       // raw ring slots
   static constexpr int D_ROW = 3 * ROWB;   // three kx-shifted copies of a dout row
   static constexpr int D_PART = TY * D_ROW;
-  static constexpr int D_OFF = NP * X_PART;
-  static constexpr int BUF = (D_OFF + NP * D_PART + 1023) / 1024 * 1024;
+  static constexpr int BUF = (NP * D_PART + 1023) / 1024 * 1024;   // dout operand (B) only
+  static constexpr int A_BUF_COLS = NP * 16;
   static constexpr int RAW_OFF = NB * BUF;
   // raw_full[NR], raw_empty[NR], op_full[NB], op_free[NB], d_full, d_empty
   static constexpr int BAR_OFF = RAW_OFF + NR * RAW_SLOT;
@@ -119,11 +123,12 @@ __device__ __forceinline__ void store8(uint32_t dst, uint32_t part_stride, const
   for (int p = 0; p < NP; ++p) st_shared_v4(dst + p * part_stride, w[0][p], w[1][p], w[2][p], w[3][p]);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+// D (TMEM) += A (TMEM, 128 lanes x 16 bf16) * B (shared-memory descriptor)^T
+__device__ __forceinline__ void mma_bf16_ta(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(IDESC), "r"(acc)
       : "memory");
 }
 
@@ -199,10 +204,16 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
   const long long stride = gridDim.x;
   const int n_tiles = (int)max(0ll, (P.n_tiles - blockIdx.x + stride - 1) / stride);
   if (warp < L::MMA_WARP) {
-    // ---- converters: raw slot -> split-bf16 core matrices (operand buffer)
-    const int u = tid;
-    const int c8 = u & 7, kc = (u >> 3) & 3, cg = (u >> 5) & 3, r = u >> 7;   // x unit; d unit if u < D_UNITS
-    const int c = cg * 8 + c8;
+    // ---- converters: raw slot -> split-bf16 operands.  Warps 0-3 and 12-15:
+    //      x row r = warp & 3 (TMEM lane quarter = ky'), lane = channel,
+    //      pixels 0-15 / 16-31 into the A operand in TMEM.  Warps 4-11: the
+    //      256 dout units into the B core matrices in shared memory.
+    const bool xw = warp < 4 || warp >= 12;
+    const int xh = warp >= 12 ? 1 : 0;         // pixel half of the x row
+    const int u = tid - 128;
+    const int c8 = u & 7, kc = (u >> 3) & 3, cg = (u >> 5) & 3, yy = u >> 7;   // dout unit (u < D_UNITS)
+    const int c = xw ? lane : cg * 8 + c8;
+    const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL + xh * 8;
     float dbacc = 0.f;
     for (int i_t = 0; i_t < n_tiles; ++i_t) {
       const int slot = i_t % L::NR, q = i_t % NB;
@@ -212,20 +223,33 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
         if (i_t >= NB) mbar_wait(op_free0 + 8 * q, ((i_t / NB) - 1) & 1);
       }
       __syncwarp();
+      tc_fence_after();
       const long long tl1 = clock64();
       const uint32_t raw = sbase + L::RAW_OFF + slot * RAW_SLOT;
       const uint32_t buf = sbase + q * L::BUF;
-      {
-        // x: swizzled row R = r * 32 + c, logical 16-B chunk j at j ^ (R & 7) = j ^ c8
-        const uint32_t row = raw + (uint32_t)(r * C + c) * 128;
-        const float4 a = ld_shared_f4(row + (((2 * kc) ^ c8) << 4));
-        const float4 b = ld_shared_f4(row + (((2 * kc + 1) ^ c8) << 4));
-        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        store8<NP>(buf + r * ROWB + cg * CGB + kc * 128 + c8 * 16, L::X_PART, v);
-      }
-      if (u < D_UNITS) {
-        // dout row (yy = r): box pixel e = p - (x0 - 4); values p = x0 + 8 kc - 1 .. + 8 are e = 8 kc + 3 .. 8 kc + 12
-        const uint32_t row = raw + RAW_X + (uint32_t)(r * C + c) * (DBOX * 4) + kc * 32;
+      if (xw) {
+        // swizzled raw row R = r * 32 + c: logical 16-B chunk j at j ^ (c & 7)
+        const uint32_t row = raw + (uint32_t)((warp & 3) * C + c) * 128;
+        uint32_t w[NP][8];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = xh * 4 + jj;
+          const float4 f = ld_shared_f4(row + ((j ^ (c & 7)) << 4));
+          uint32_t p0[NP], p1[NP];
+          split_pair<NP>(f.x, f.y, p0);
+          split_pair<NP>(f.z, f.w, p1);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            w[p][2 * jj] = p0[p];
+            w[p][2 * jj + 1] = p1[p];
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) tmem_st8u(a_lane + q * L::A_BUF_COLS + p * 16, w[p]);
+        tmem_wait_st();
+      } else if (u < D_UNITS) {
+        // dout row yy: box pixel e = p - (x0 - 4); values p = x0 + 8 kc - 1 .. + 8 are e = 8 kc + 3 .. 8 kc + 12
+        const uint32_t row = raw + RAW_X + (uint32_t)(yy * C + c) * (DBOX * 4) + kc * 32;
         const float4 a = ld_shared_f4(row), b = ld_shared_f4(row + 16), e = ld_shared_f4(row + 32),
                      f = ld_shared_f4(row + 48);
         const float dv[10] = {a.w, b.x, b.y, b.z, b.w, e.x, e.y, e.z, e.w, f.x};
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
         uint32_t ev[5][NP];
 #pragma unroll
         for (int i = 0; i < 5; ++i) split_pair<NP>(dv[2 * i], dv[2 * i + 1], ev[i]);
-        const uint32_t dst = buf + L::D_OFF + r * L::D_ROW + cg * CGB + kc * 128 + c8 * 16;
+        const uint32_t dst = buf + yy * L::D_ROW + cg * CGB + kc * 128 + c8 * 16;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           st_shared_v4(dst + p * L::D_PART, ev[1][p], ev[2][p], ev[3][p], ev[4][p]);
@@ -246,6 +270,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
         }
       }
       fence_proxy_async();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(raw_empty0 + 8 * slot);
@@ -253,7 +278,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
       }
       if (warp == 0) WTL(0, i_t, tl0, tl1, 0);
     }
-    if (u < D_UNITS) atomicAdd(&db_s[c], dbacc);
+    if (!xw && u < D_UNITS) atomicAdd(&db_s[c], dbacc);
   } else if (warp == L::TMA_WARP) {
     // ---- producer: raw boxes of tile i into slot i % NR
     if (lane == 0) {
@@ -293,17 +318,18 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
       tc_fence_after();
       if (lane == 0) {
         const uint32_t buf = sbase + q * L::BUF;
-        // K-major, no swizzle: K core matrices 128 B apart, 8-row groups CGB apart
+        // B: K-major, no swizzle: K core matrices 128 B apart, 8-row groups
+        // CGB apart; A: part pa, K-step ks at TMEM column +pa*16 + ks*8
         const uint64_t d0 = umma_desc(buf, 128, CGB);
+        const uint32_t a0 = tmem + A_COL + q * L::A_BUF_COLS;
 #pragma unroll
         for (int ks = 0; ks < WT / 16; ++ks)
 #pragma unroll
           for (int pr = 0; pr < L::NPROD; ++pr) {
             constexpr int pa_tab[6] = {0, 0, 1, 0, 1, 2}, pb_tab[6] = {0, 1, 0, 2, 1, 0};
-            const uint32_t ao = (pa_tab[pr] * L::X_PART + ks * 256) >> 4;
-            const uint32_t bo = (L::D_OFF + pb_tab[pr] * L::D_PART + ks * 256) >> 4;
+            const uint32_t bo = (pb_tab[pr] * L::D_PART + ks * 256) >> 4;
             const bool first = chain_start && ks == 0 && pr == 0;
-            mma_bf16(tmem + D_COL, d0 + ao, d0 + bo, first ? 0u : 1u);
+            mma_bf16_ta(tmem + D_COL, a0 + pa_tab[pr] * 16 + ks * 8, d0 + bo, first ? 0u : 1u);
           }
         tc_commit(op_free0 + 8 * q);
         if (chain_end) tc_commit(d_full);
