@@ -237,7 +237,29 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
         for (int i = 0; i < HC; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
       }
     };
-    load_row(A);
+    // this thread's 16 channels of an input row -> three bf16 parts in the
+    // row's A buffer (visible to the MMAs after the next CTA barrier)
+    auto split_row = [&](int row) {
+      const uint32_t dst = sbase + A_OFF + (row & 1) * NPART * ROW + (2 * half) * PLANE + l * 16;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        uint32_t w[3][4];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) {
+          __nv_bfloat16 a0, a1, a2, c0, c1, c2;
+          split3(xin[8 * g + 2 * k2], a0, a1, a2);
+          split3(xin[8 * g + 2 * k2 + 1], c0, c1, c2);
+          w[0][k2] = pack_bf2(a0, c0);
+          w[1][k2] = pack_bf2(a1, c1);
+          w[2][k2] = pack_bf2(a2, c2);
+        }
+#pragma unroll
+        for (int pp = 0; pp < 3; ++pp)
+          st_shared_v4(dst + pp * ROW + g * PLANE, w[pp][0], w[pp][1], w[pp][2], w[pp][3]);
+      }
+      fence_proxy_async();
+    };
+    load_row(A);                       // split in the first iteration (r = A-2)
     int tm3 = ((A - 3) % 3 + 3) % 3;   // slot of row r-1 at t = A-2
     for (int r = A - 2; r <= Bn; ++r) {
       const int d = r - 1, e = r + 2, slot = tm3;
@@ -269,29 +291,12 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
         }
       }
       if (e >= A && e < Bn) tmem_st16_zero(taddr);
-      // ---- 4. input row r+1 -> hi / lo A planes, then issue its 36 MMAs
+      // ---- 4. issue MMA(r+1): its input row was split into A buffer (r+1)&1
+      //         one step earlier, right after MMA(r) was issued
       const int rn = r + 1;
       const bool issue = rn >= A && rn < Bn;
       if (issue) {
         const int q = rn & 1;
-        const uint32_t dst = sbase + A_OFF + q * NPART * ROW + (2 * half) * PLANE + l * 16;
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          uint32_t w[3][4];
-#pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) {
-            __nv_bfloat16 a0, a1, a2, c0, c1, c2;
-            split3(xin[8 * g + 2 * k2], a0, a1, a2);
-            split3(xin[8 * g + 2 * k2 + 1], c0, c1, c2);
-            w[0][k2] = pack_bf2(a0, c0);
-            w[1][k2] = pack_bf2(a1, c1);
-            w[2][k2] = pack_bf2(a2, c2);
-          }
-#pragma unroll
-          for (int pp = 0; pp < 3; ++pp)
-            st_shared_v4(dst + pp * ROW + g * PLANE, w[pp][0], w[pp][1], w[pp][2], w[pp][3]);
-        }
-        fence_proxy_async();
         tmem_wait_st();
         tc_fence_before();
         __syncthreads();
@@ -306,7 +311,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
           __syncwarp();
         }
       }
-      // ---- 5. epilogue of row d (overlaps the MMAs), 6. prefetch the next row
+      // ---- 5. input row r+2 -> the three bf16 A planes of buffer (r+2)&1
+      //         (last read by MMA(r), retired in step 1), off the path from
+      //         MMA(r)'s completion to MMA(r+1)'s issue
+      if (r + 2 >= A && r + 2 < Bn) split_row(r + 2);
+      // ---- 6. epilogue of row d (overlaps the MMAs), 7. prefetch the row after
       if (drain && d >= R0 && d < R1 && lane_valid) {
         const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
 #pragma unroll
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
           P.out[idx] = y;
         }
       }
-      if (issue) load_row(rn + 1);
+      if (r + 2 >= A && r + 2 < Bn) load_row(r + 3);
     }
   }
   tc_fence_before();
