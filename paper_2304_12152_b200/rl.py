@@ -306,25 +306,15 @@ def draw_batch(dataset, cfg, rng, device=None, keep=None):
     return crops, gaussian_maps_device(starts, size, size, device=device)
 
 
-def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None):
-    """One optimisation step (rl.py:232-278); returns the diagnostics row.
-
-    group: torch.distributed process group for data parallelism (default:
-    the world group when initialised).  signal_override: test hook -- a
-    callable(sample_index, m) -> LE signal (float64 (H,W)) replacing the GPU
-    estimator, used by staged parity tests."""
+def _prepare_step(dataset, cfg, rng, dev, rank, world):
+    """Every RNG draw of one train_step, in the reference's order (crops and
+    noise maps, action uniforms, gray levels and their noise maps), and this
+    rank's inputs on the device.  Nothing here depends on the network."""
     torch = _torch()
-    _lib.require_cuda()
-    rank, world = _dist_info(group)
-    dev = net.device
     size, bs = cfg.crop_size, cfg.batch_size
-    mcfg = cfg.metric_config()
     lo, hi = shard_range(bs, rank, world)
+    start = rng.state_words()
     crops, noises = draw_batch(dataset, cfg, rng, device=dev, keep=range(lo, hi))
-    grad = torch.zeros(net.num_params(), dtype=torch.float64, device=dev)
-    # reward, bin_gap, l_as sums, non-finite flags (one all-reduce, one
-    # read-back per step)
-    stats = torch.zeros(4, dtype=torch.float64, device=dev)
     # RNG states at the reference's two forwards: a non-finite logit is
     # detected once per step (no wait per forward) and raised with the
     # stream where the reference's forward (nn.py:147-148) would have raised
@@ -338,13 +328,12 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     ud = rng.uniforms_device((hi - lo) * n, device=dev).view(hi - lo, size, size) if hi > lo else None
     rng.jump((bs - hi) * n)
     run_aniso = cfg.w_a != 0.0 and (cfg.levels == 2 or cfg.multitone_anisotropy)
-    nm, ng = hi - lo, 0
-    inputs = []
+    nm, ng, ba = hi - lo, 0, cfg.anisotropy_batch_size or bs
+    inputs, cd = [], None
     if nm:
         cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory().to(dev, non_blocking=True)
         inputs.append(torch.stack((cd, noises), dim=1))
     if run_aniso:
-        ba = cfg.anisotropy_batch_size or bs
         grays = [rng.uniform() for _ in range(ba)]
         glo, ghi = shard_range(ba, rank, world)
         # the gray images' noise maps follow each other in the stream: this
@@ -362,6 +351,56 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
             gd = torch.tensor([grays[i] for i in range(glo, ghi)], dtype=torch.float32)
             gd = gd.pin_memory().to(dev, non_blocking=True)[:, None, None].expand(-1, size, size)
             inputs.append(torch.stack((gd, znoise), dim=1))
+    return {"start": start, "end": rng.state_words(), "rng_at_fwd": rng_at_fwd, "lo": lo, "hi": hi,
+            "nm": nm, "ng": ng, "ba": ba, "cd": cd, "ud": ud, "inputs": inputs}
+
+
+# the next step's draws and inputs, prepared while the GPU runs this step
+# (one entry; used only if the caller's RNG is where this step left it)
+_next_step = {}
+
+
+def _take_prepared(dataset, cfg, rng, dev, rank, world):
+    key = (id(dataset), cfg, str(dev), rank, world)
+    prep = _next_step.pop("prep", None)
+    if prep is not None and _next_step.pop("key", None) == key and prep["start"] == rng.state_words():
+        rng.set_state_words(prep["end"])
+        return prep
+    _next_step.clear()
+    return _prepare_step(dataset, cfg, rng, dev, rank, world)
+
+
+def _prefetch_next(dataset, cfg, rng, dev, rank, world):
+    ahead = Rng(0)
+    ahead.set_state_words(rng.state_words())
+    _next_step["prep"] = _prepare_step(dataset, cfg, ahead, dev, rank, world)
+    _next_step["key"] = (id(dataset), cfg, str(dev), rank, world)
+
+
+def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None, prefetch=True):
+    """One optimisation step (rl.py:232-278); returns the diagnostics row.
+
+    group: torch.distributed process group for data parallelism (default:
+    the world group when initialised).  signal_override: test hook -- a
+    callable(sample_index, m) -> LE signal (float64 (H,W)) replacing the GPU
+    estimator, used by staged parity tests.  prefetch: draw the next step's
+    batch (from a copy of the RNG stream) while the GPU runs this one; the
+    next call uses it only if its RNG is exactly where this step left it."""
+    torch = _torch()
+    _lib.require_cuda()
+    rank, world = _dist_info(group)
+    dev = net.device
+    bs = cfg.batch_size
+    mcfg = cfg.metric_config()
+    prep = _take_prepared(dataset, cfg, rng, dev, rank, world)
+    lo, nm, ng, ba = prep["lo"], prep["nm"], prep["ng"], prep["ba"]
+    cd, ud, inputs, rng_at_fwd = prep["cd"], prep["ud"], prep["inputs"], prep["rng_at_fwd"]
+    size = cfg.crop_size
+    run_aniso = cfg.w_a != 0.0 and (cfg.levels == 2 or cfg.multitone_anisotropy)
+    grad = torch.zeros(net.num_params(), dtype=torch.float64, device=dev)
+    # reward, bin_gap, l_as sums, non-finite flags (one all-reduce, one
+    # read-back per step)
+    stats = torch.zeros(4, dtype=torch.float64, device=dev)
     # one forward + one backward over this rank's MARL crops and gray images
     # (the reference's two forwards, batched: samples are independent and the
     # parameters do not change in between); sample b's non-finite flag
@@ -404,6 +443,8 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
         stats[2] += loss.sum()
     if dps:
         net.backward_device(dps[0] if len(dps) == 1 else torch.cat(dps), grad)
+    if prefetch:
+        _prefetch_next(dataset, cfg, rng, dev, rank, world)
     stats[3] = (nonfinite[:nm].amax().double() if nm else 0.0) + \
         2.0 * (nonfinite[nm:nm + ng].amax().double() if ng else 0.0)
     allreduce_sum_(grad, stats, group=group)   # the step's one exchange
