@@ -360,8 +360,16 @@ def _prepare_step(dataset, cfg, rng, dev, rank, world):
 _next_step = {}
 
 
+def _dataset_key(dataset):
+    # identity of the image list and of each array's buffer (an image
+    # replaced between steps invalidates the prefetched batch)
+    return (id(dataset), len(dataset),
+            tuple((id(a), a.__array_interface__["data"][0] if hasattr(a, "__array_interface__") else 0)
+                  for a in dataset))
+
+
 def _take_prepared(dataset, cfg, rng, dev, rank, world):
-    key = (id(dataset), cfg, str(dev), rank, world)
+    key = (_dataset_key(dataset), cfg, str(dev), rank, world)
     prep = _next_step.pop("prep", None)
     if prep is not None and _next_step.pop("key", None) == key and prep["start"] == rng.state_words():
         rng.set_state_words(prep["end"])
@@ -374,7 +382,7 @@ def _prefetch_next(dataset, cfg, rng, dev, rank, world):
     ahead = Rng(0)
     ahead.set_state_words(rng.state_words())
     _next_step["prep"] = _prepare_step(dataset, cfg, ahead, dev, rank, world)
-    _next_step["key"] = (id(dataset), cfg, str(dev), rank, world)
+    _next_step["key"] = (_dataset_key(dataset), cfg, str(dev), rank, world)
 
 
 def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None, prefetch=True):
@@ -385,7 +393,9 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     callable(sample_index, m) -> LE signal (float64 (H,W)) replacing the GPU
     estimator, used by staged parity tests.  prefetch: draw the next step's
     batch (from a copy of the RNG stream) while the GPU runs this one; the
-    next call uses it only if its RNG is exactly where this step left it."""
+    next call uses it only if its RNG is exactly where this step left it and
+    the dataset holds the same arrays (pass prefetch=False if image contents
+    are edited in place between steps)."""
     torch = _torch()
     _lib.require_cuda()
     rank, world = _dist_info(group)

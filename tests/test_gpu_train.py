@@ -196,3 +196,45 @@ def test_train_step_nonfinite_raises_before_update():
     assert np.array_equal(net.flat_values(), p0, equal_nan=True)
     assert adam.t == 0
     assert rng.state_words() == expect.state_words()
+
+
+def test_train_step_prefetch_is_transparent():
+    """train_step prepares the next step's batch from a copy of the RNG
+    stream while the GPU works; with or without it, three steps draw the
+    same stream (RNG state bit for bit) and give the same parameters and
+    diagnostics (to the run-to-run noise of atomic sums), and a dataset
+    image replaced between steps (or an RNG moved by the caller) makes the
+    next step draw afresh."""
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    g = golden("train.npz")
+    cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
+                         anisotropy_batch_size=2, hvs_model="gaussian")
+
+    def run(prefetch, swap=False, poke=False):
+        ds = list(g["mini_ds"])
+        net = PolicyNetwork(8, 2)
+        adam = Adam(net.params())
+        rng = Rng(cfg.seed)
+        net.init_params(rng)
+        rows = []
+        for t in range(3):
+            if swap and t == 1:
+                ds[0] = ds[0][::-1].copy()        # a different image in the same list
+            if poke and t == 2:
+                rng.uniform()                      # the caller draws from the stream
+            rows.append(rl.train_step(net, adam, ds, cfg, rng, t, prefetch=prefetch))
+        return net.flat_values(), rows, rng.state_words()
+
+    # gradients are summed with fp64 atomics (order varies run to run: two
+    # runs of the same path differ by ~1e-18); the draws must match exactly
+    for kw in ({}, {"swap": True}, {"poke": True}):
+        a = run(True, **kw)
+        b = run(False, **kw)
+        assert a[2] == b[2], kw
+        assert np.max(np.abs(a[0] - b[0])) < 1e-15, kw
+        for ra, rb in zip(a[1], b[1]):
+            for key in ("reward", "l_as", "bin_gap"):
+                assert abs(ra[key] - rb[key]) <= 1e-12 * max(1.0, abs(rb[key])), (kw, key)
+            assert ra["lr"] == rb["lr"] and ra["iteration"] == rb["iteration"]
