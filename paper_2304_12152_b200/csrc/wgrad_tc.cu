@@ -132,9 +132,6 @@ __device__ __forceinline__ void mma_bf16_ta(uint32_t d, uint32_t a_tmem, uint64_
       : "memory");
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
                                             uint32_t bar) {
   asm volatile(
@@ -398,17 +395,6 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
   }
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void *ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
 // (W, C, H, B) view of an NCHW fp32 tensor; box (bw, 32, bh, 1)
 static int make_map(CUtensorMap *map, const float *base, int B, int H, int W, int bw, int bh, bool swz) {
   auto enc = tensor_map_encoder();
