@@ -1,11 +1,12 @@
-import ctypes as C, sys, numpy as np, torch
+import ctypes as C, os, sys, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2304_12152_b200 import _lib, synth
 from paper_2304_12152_b200.imagecore import Rng
 from paper_2304_12152_b200.nn import PolicyNetwork
 lib = _lib.load()
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-net = PolicyNetwork(32, 16); net.init_params(Rng(0), std=0.01)
+NB = int(os.environ.get("HT_NB", "16"))
+net = PolicyNetwork(32, NB); net.init_params(Rng(0), std=0.01)
 c = torch.from_numpy(synth.config_batch(B, 512, 512, seed=2)).cuda()
 z = torch.randn(B, 512, 512, device='cuda')
 h = torch.empty((B, 512, 512), dtype=torch.uint8, device='cuda')
