@@ -222,6 +222,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    _lib.call("ht_timing_reserve", 16 * args.steps)
     _lib.call("ht_timing_enable", 1)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

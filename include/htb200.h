@@ -130,6 +130,9 @@ int ht_last_launch_count(int *count);
  * returns (tag, ms) per launch since the last read.  tag = 100*has_conv_in +
  * 10*blocks_in_pass + has_conv_out. */
 int ht_timing_enable(int on);
+/* Pre-creates n (begin, end) event pairs for the hooks (no event creation
+ * inside a timed region). */
+int ht_timing_reserve(int n);
 int ht_timing_read(int *tags, float *ms, int max, int *count);
 
 /* Training convolutions (nn.py:46-77): 0 = the 32 -> 32 convs of the residual

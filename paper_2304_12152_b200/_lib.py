@@ -43,6 +43,7 @@ SIGNATURES = {
                      _i, _vp],
     "ht_last_launch_count": [_ip],
     "ht_timing_enable": [_i],
+    "ht_timing_reserve": [_i],
     "ht_timing_read": [_vp, _vp, _i, _ip],
     "ht_set_train_conv_impl": [_i],
     "ht_set_wgrad_parts": [_i],

@@ -103,6 +103,16 @@ int ht_timing_enable(int on) {
   ht::g_timing = on != 0;
   return HT_OK;
 }
+// Pre-creates n event pairs for the timing hooks, so a timed region does not
+// pay for event creation (the first timed step would otherwise).
+int ht_timing_reserve(int n) {
+  while ((int)ht::g_event_pool.size() < 2 * n) {
+    cudaEvent_t e;
+    HT_CUDA(cudaEventCreate(&e));
+    ht::g_event_pool.push_back(e);
+  }
+  return HT_OK;
+}
 // Copies up to `max` (tag, milliseconds) pairs recorded since the last read
 // (synchronises on the recorded events), then clears the record.
 int ht_timing_read(int *tags, float *ms, int max, int *count) {
