@@ -48,8 +48,8 @@ constexpr int W_BYTES = NPART * 3 * 2 * TILE;
 constexpr int A_OFF = W_BYTES;
 constexpr int A_BYTES = 2 * NPART * ROW;    // 2 buffers x 3 parts
 constexpr int BAR_OFF = A_OFF + A_BYTES;
-constexpr int SMEM = BAR_OFF + 16 + 16;
-constexpr int CORR_COL = 3 * 3 * C;   // TMEM column of the correction ring
+constexpr int SMEM = BAR_OFF + 16 + 16;   // acc_full[2], TMEM address
+constexpr int NRING = 4;              // TMEM rings (input row mod 4), 96 columns each
 constexpr int NTHR = 256;             // 2 channel halves x 4 lane quarters
 constexpr int HC = C / 2;             // channels per thread
 constexpr uint32_t IDESC_BF16 =
@@ -67,96 +67,94 @@ __device__ __forceinline__ uint32_t pack_bf2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
 }
 
-// One input row: for kx in 0..2, K-half kh in 0..1 (16 channels) and the six
-// split products (i, j) with i + j <= 2: D[128 x 96] += A_i[128 x 16] * B_j[96 x 16]^T.
-// The main products (0, 0) go to this input row's own ring d_main (the first
-// overwrites it: no re-init), the five smaller correction products to the
-// shared ring d_corr -- short accumulation chains for the large terms keep
-// the tensor core's fp32 accumulation error at the SIMT level.
-// Descriptors are the six bases plus immediate offsets (16-B units).
-__device__ __forceinline__ void mma36_row(uint32_t d_main, uint32_t d_corr, uint64_t a0, uint64_t a1,
-                                          uint64_t a2, uint64_t b0, uint64_t b1, uint64_t b2,
-                                          uint32_t bar_acc) {
+// One input row into its own TMEM ring: for kx in 0..2, K-half kh in 0..1 (16
+// channels) and the six split products (i, j) with i + j <= 2:
+// D[128 x 96] += A_i[128 x 16] * B_j[96 x 16]^T.  The thirty small correction
+// products go first (the first overwrites the ring: no re-init), the six
+// main products (0, 0) last, so the large partial sums see only six fp32
+// accumulation steps -- the tensor core's accumulation error stays at the
+// SIMT level.  Descriptors are the six bases plus immediate offsets (16-B units).
+__device__ __forceinline__ void mma36_row(uint32_t d, uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b0,
+                                          uint64_t b1, uint64_t b2, uint32_t bar_acc) {
   asm volatile(
       "{\n\t.reg .pred e, p, z;\n\t.reg .b64 ta, tb;\n\t"
       "setp.ne.b32 p, 1, 0;\n\t"
       "setp.ne.b32 z, 0, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
+      "add.s64 ta, %1, -1;\n\tadd.s64 tb, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, z;\n\t"
+      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, -1;\n\tadd.s64 tb, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, -1;\n\tadd.s64 tb, %5, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, z;\n\t"
-      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %6, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, -1;\n\tadd.s64 tb, %5, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, -1;\n\tadd.s64 tb, %7, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, -1;\n\tadd.s64 tb, %6, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, -1;\n\tadd.s64 tb, %5, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, -1;\n\tadd.s64 tb, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 255;\n\tadd.s64 tb, %5, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %4, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 255;\n\tadd.s64 tb, %6, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, 255;\n\tadd.s64 tb, %5, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %6, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 255;\n\tadd.s64 tb, %5, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 255;\n\tadd.s64 tb, %7, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 255;\n\tadd.s64 tb, %6, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, 255;\n\tadd.s64 tb, %5, 320;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, 255;\n\tadd.s64 tb, %4, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 0;\n\tadd.s64 tb, %5, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %4, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 0;\n\tadd.s64 tb, %6, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, 0;\n\tadd.s64 tb, %5, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %6, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 0;\n\tadd.s64 tb, %5, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 0;\n\tadd.s64 tb, %7, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 0;\n\tadd.s64 tb, %6, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, 0;\n\tadd.s64 tb, %5, 640;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, 0;\n\tadd.s64 tb, %4, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 256;\n\tadd.s64 tb, %5, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %4, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 256;\n\tadd.s64 tb, %6, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, 256;\n\tadd.s64 tb, %5, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %6, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 256;\n\tadd.s64 tb, %5, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 256;\n\tadd.s64 tb, %7, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 256;\n\tadd.s64 tb, %6, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, 256;\n\tadd.s64 tb, %5, 960;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, 256;\n\tadd.s64 tb, %4, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %4, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 1;\n\tadd.s64 tb, %6, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %6, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 1;\n\tadd.s64 tb, %7, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 1;\n\tadd.s64 tb, %6, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, 1;\n\tadd.s64 tb, %5, 1280;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, 1;\n\tadd.s64 tb, %4, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %4, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 257;\n\tadd.s64 tb, %6, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
       "add.s64 ta, %2, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %6, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %2, 257;\n\tadd.s64 tb, %7, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %3, 257;\n\tadd.s64 tb, %6, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "add.s64 ta, %4, 257;\n\tadd.s64 tb, %5, 1600;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ta, tb, %8, p;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}"
-      ::"r"(d_main), "r"(d_corr), "l"(a0), "l"(a1), "l"(a2), "l"(b0), "l"(b1), "l"(b2), "r"(IDESC_BF16),
-        "r"(bar_acc)
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %3, 257;\n\tadd.s64 tb, %4, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, -1;\n\tadd.s64 tb, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 255;\n\tadd.s64 tb, %4, 320;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 0;\n\tadd.s64 tb, %4, 640;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 256;\n\tadd.s64 tb, %4, 960;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 1;\n\tadd.s64 tb, %4, 1280;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "add.s64 ta, %1, 257;\n\tadd.s64 tb, %4, 1600;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %7, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}"
+      ::"r"(d), "l"(a0), "l"(a1), "l"(a2), "l"(b0), "l"(b1), "l"(b2), "r"(IDESC_BF16), "r"(bar_acc)
       : "memory");
 }
 
@@ -173,10 +171,12 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t acc_full = sbase + BAR_OFF;
+  // MMA(x) commits to acc_full[x & 1]: two batches can be in flight
+  auto acc_full = [&](int x) { return sbase + BAR_OFF + 8u * (uint32_t)(x & 1); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 16);
   if (tid == 0) {
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full(0), 1);
+    mbar_init(acc_full(1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // weights: OIHW fp32 -> three bf16 parts, UMMA tiles [part][kx][kh] of 160
@@ -259,45 +259,23 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       }
       fence_proxy_async();
     };
+    // Input row x's products go to TMEM ring x mod 4 (three 32-column slots:
+    // output rows mod 3); output row d is the sum of the slots d mod 3 of the
+    // rings of input rows d-1, d, d+1.  Step r issues MMA(r+1) first -- its
+    // ring last held row r-3, drained a step earlier -- and only then waits
+    // for MMA(r), so the tensor pipe always has the next row queued while
+    // the threads drain row r-1, split row r+2 and store row r-1.
     load_row(A);                       // split in the first iteration (r = A-2)
     int tm3 = ((A - 3) % 3 + 3) % 3;   // slot of row r-1 at t = A-2
     for (int r = A - 2; r <= Bn; ++r) {
-      const int d = r - 1, e = r + 2, slot = tm3;
+      const int d = r - 1, slot = tm3;
       tm3 = tm3 == 2 ? 0 : tm3 + 1;
-      // ---- 1. MMA(r) done (retires every earlier MMA and input buffer)
-      if (r >= A && r < Bn) {
-        if (lane == 0) mbar_wait(acc_full, ph_acc & 1);
-        ph_acc ^= 1u;
-        __syncwarp();
-        tc_fence_after();
-      }
-      // ---- 2. finished output row d -> registers, 3. slot re-init for row e
-      // TMEM: main rings 0..2 (input row mod 3) at 96 q, correction ring at
-      // 288; output row y lives in column block y mod 3 of each ring
-      const uint32_t taddr = tlane + CORR_COL + slot * C + c0;
-      const bool drain = d >= A && d < Bn;
-      if (drain) {
-        tmem_ld16(taddr, vals);
-        // main parts of input rows d-1, d, d+1 (rings x mod 3); an input row
-        // outside [A, Bn) is zero padding: its ring holds an older row
-#pragma unroll
-        for (int k = -1; k <= 1; ++k) {
-          const int xr = d + k;
-          if (xr < A || xr >= Bn) continue;
-          float part[HC];
-          tmem_ld16(tlane + (xr % 3) * 3 * C + slot * C + c0, part);
-#pragma unroll
-          for (int i = 0; i < HC; ++i) vals[i] += part[i];
-        }
-      }
-      if (e >= A && e < Bn) tmem_st16_zero(taddr);
-      // ---- 4. issue MMA(r+1): its input row was split into A buffer (r+1)&1
-      //         one step earlier, right after MMA(r) was issued
+      // ---- 1. issue MMA(r+1): its input row was split into A buffer (r+1)&1
+      //         in the previous step (barrier: every warp's split and drain of
+      //         that step are done)
       const int rn = r + 1;
-      const bool issue = rn >= A && rn < Bn;
-      if (issue) {
+      if (rn >= A && rn < Bn) {
         const int q = rn & 1;
-        tmem_wait_st();
         tc_fence_before();
         __syncthreads();
         if (warp == 0) {
@@ -306,16 +284,41 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
           const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);       // B window for rows (r+2, r+1, r)
           const uint64_t a = adesc0 + ((A_OFF + q * NPART * ROW) >> 4);
           const uint64_t bw = bdesc0 + ((o * C * 16) >> 4);
-          mma36_row(tmem + (uint32_t)((rn % 3) * 3 * C), tmem + CORR_COL, a, a + (ROW >> 4),
-                    a + ((2 * ROW) >> 4), bw, bw + ((6 * TILE) >> 4), bw + ((12 * TILE) >> 4), acc_full);
+          mma36_row(tmem + (uint32_t)((rn % NRING) * 3 * C), a, a + (ROW >> 4), a + ((2 * ROW) >> 4), bw,
+                    bw + ((6 * TILE) >> 4), bw + ((12 * TILE) >> 4), acc_full(rn));
           __syncwarp();
         }
+      } else if (r == A - 2) {
+        __syncthreads();               // segment start: the previous segment's buffers are free
       }
-      // ---- 5. input row r+2 -> the three bf16 A planes of buffer (r+2)&1
-      //         (last read by MMA(r), retired in step 1), off the path from
-      //         MMA(r)'s completion to MMA(r+1)'s issue
+      // ---- 2. MMA(r) done (and every earlier MMA; MMA(r+1) may still run)
+      if (r >= A && r < Bn) {
+        if (lane == 0) mbar_wait(acc_full(r), (ph_acc >> (r & 1)) & 1);
+        ph_acc ^= 1u << (r & 1);
+        __syncwarp();
+        tc_fence_after();
+      }
+      // ---- 3. finished output row d -> registers: slots d mod 3 of the rings
+      //         of input rows d-1, d, d+1 (a row outside [A, Bn) is zero
+      //         padding: its ring holds an older row)
+      const bool drain = d >= A && d < Bn;
+      if (drain) {
+#pragma unroll
+        for (int i = 0; i < HC; ++i) vals[i] = 0.f;
+#pragma unroll
+        for (int k = -1; k <= 1; ++k) {
+          const int xr = d + k;
+          if (xr < A || xr >= Bn) continue;
+          float part[HC];
+          tmem_ld16(tlane + (xr % NRING) * 3 * C + slot * C + c0, part);
+#pragma unroll
+          for (int i = 0; i < HC; ++i) vals[i] += part[i];
+        }
+      }
+      // ---- 4. input row r+2 -> the three bf16 A planes of buffer (r+2)&1
+      //         (last read by MMA(r), retired in step 2)
       if (r + 2 >= A && r + 2 < Bn) split_row(r + 2);
-      // ---- 6. epilogue of row d (overlaps the MMAs), 7. prefetch the row after
+      // ---- 5. epilogue of row d (overlaps MMA(r+1)), 6. prefetch the row after
       if (drain && d >= R0 && d < R1 && lane_valid) {
         const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
 #pragma unroll
