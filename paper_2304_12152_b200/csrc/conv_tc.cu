@@ -48,9 +48,18 @@ constexpr int W_BYTES = NPART * 3 * 2 * TILE;
 constexpr int A_OFF = W_BYTES;
 constexpr int A_BYTES = 2 * NPART * ROW;    // 2 buffers x 3 parts
 constexpr int BAR_OFF = A_OFF + A_BYTES;
-constexpr int SMEM = BAR_OFF + 16 + 16;   // acc_full[2], TMEM address
+// barriers acc_full[2], ready[2], stg_full[2], TMEM address
+constexpr int STG_OFF = BAR_OFF + 128;
+// one TMA box: 132 px x 32 channels fp32 ([ch][px]); a box's first column
+// must be a multiple of 4 (16 B), so it starts up to 3 px left of lane 0
+constexpr int BOXW = M + 4;
+constexpr int BOX = BOXW * C * 4;
+constexpr int STG_SLOT = 2 * BOX;     // a strip row spans at most two images (W + 1 >= 128)
+constexpr int SMEM_LDG = STG_OFF;
+constexpr int SMEM_TMA = STG_OFF + 2 * STG_SLOT;
 constexpr int NRING = 4;              // TMEM rings (input row mod 4), 96 columns each
-constexpr int NTHR = 256;             // 2 channel halves x 4 lane quarters
+constexpr int NWORK = 256;            // worker threads: 2 channel halves x 4 lane quarters
+constexpr int NTHR = NWORK + 32;      // + one MMA-issuer warp
 constexpr int HC = C / 2;             // channels per thread
 constexpr uint32_t IDESC_BF16 =
     (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -158,7 +167,17 @@ __device__ __forceinline__ void mma36_row(uint32_t d, uint64_t a0, uint64_t a1, 
       : "memory");
 }
 
+#ifdef CT_TL
+// debug timeline of CTA 0, warp 0 lane 0: per step (r, after barrier+issue,
+// MMA(r) seen, drained, split, stored+loaded)
+__device__ long long g_ctl[4096][6];
+#define CTL(k) do { if (blockIdx.x == 0 && threadIdx.x == 0 && ctl_n < 4096) g_ctl[ctl_n][k] = clock64(); } while (0)
+#else
+#define CTL(k) do {} while (0)
+#endif
+
 struct ConvParams {
+  CUtensorMap tm_x;  // TX: x as (W, C, H, B) fp32, box 128 x 32 x 1 x 1
   const float *x, *w, *bias, *mask, *resid;
   float *out;
   int B, H, W, VW, relu;
@@ -166,6 +185,19 @@ struct ConvParams {
   long long chunk;   // strip-rows per CTA (strip-major)
 };
 
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+// TX: input rows arrive by TMA (issued two rows ahead by the issuer warp) into
+// a two-slot staging ring instead of per-thread loads -- an LDG still in
+// flight at a split's proxy fence (a CTA memory barrier) would stall it.
+template <bool TX>
 __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant__ ConvParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -173,10 +205,18 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
   const uint32_t sbase = smem_u32(smem);
   // MMA(x) commits to acc_full[x & 1]: two batches can be in flight
   auto acc_full = [&](int x) { return sbase + BAR_OFF + 8u * (uint32_t)(x & 1); };
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 16);
+  // ready[x & 1]: the 8 worker warps split input row x (and drained the row
+  // whose ring MMA(x) reuses) -- the issuer warp may issue MMA(x)
+  auto ready = [&](int x) { return sbase + BAR_OFF + 16 + 8u * (uint32_t)(x & 1); };
+  auto stg_full = [&](int x) { return sbase + BAR_OFF + 32 + 8u * (uint32_t)(x & 1); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 48);
   if (tid == 0) {
     mbar_init(acc_full(0), 1);
     mbar_init(acc_full(1), 1);
+    mbar_init(ready(0), NWORK / 32);
+    mbar_init(ready(1), NWORK / 32);
+    mbar_init(stg_full(0), 1);
+    mbar_init(stg_full(1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // weights: OIHW fp32 -> three bf16 parts, UMMA tiles [part][kx][kh] of 160
@@ -216,8 +256,63 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
   const long long range = P.H;
   const long long q0 = (long long)blockIdx.x * P.chunk;
   const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * range);
-  uint32_t ph_acc = 0;
+  if (warp == NWORK / 32) {
+    // ---- MMA issuer: MMA(x) for every input row x of every segment, as soon
+    //      as the workers have split row x and drained the row whose ring it
+    //      overwrites.  Blocking on a full tensor-pipe queue here costs the
+    //      workers nothing (they never issue).
+    uint32_t ph_rdy = 0;
+    for (long long qq = q0; qq < q1;) {
+      const int s = (int)(qq / range);
+      const long long end = min(q1, (long long)(s + 1) * range);
+      const int R0 = (int)(qq - (long long)s * range), R1 = (int)(end - (long long)s * range);
+      qq = end;
+      const int A = max(R0 - 1, 0), Bn = min(R1 + 1, P.H);
+      // TX: input row x of this strip -> staging slot x & 1 (one box per image
+      // the strip touches; out-of-image pixels arrive as zeros)
+      const int v0 = s * S - 1, b0 = max(v0, 0) / (P.W + 1);
+      auto tma_row = [&](int x) {
+        if (lane == 0) {
+          const int nbox = b0 + 1 < P.B ? 2 : 1;
+          mbar_expect_tx(stg_full(x), nbox * BOX);
+          for (int k = 0; k < nbox; ++k)
+            tma_load_4d(sbase + STG_OFF + (x & 1) * STG_SLOT + k * BOX, &P.tm_x, (v0 - (b0 + k) * (P.W + 1)) & ~3, 0, x,
+                        b0 + k, stg_full(x));
+        }
+      };
+      if constexpr (TX) {
+        tma_row(A);
+        if (A + 1 < Bn) tma_row(A + 1);
+      }
+      for (int x = A; x < Bn; ++x) {
+        if (lane == 0) mbar_wait(ready(x), (ph_rdy >> (x & 1)) & 1);
+        ph_rdy ^= 1u << (x & 1);
+        __syncwarp();
+        // row x was split: its staging slot takes row x+2 (before the MMAs,
+        // whose issue can block on a full tensor-pipe queue)
+        if constexpr (TX) {
+          if (x + 2 < Bn) tma_row(x + 2);
+        }
+        __syncwarp();
+        tc_fence_after();
+        const int xm3 = x % 3;
+        const int o = xm3 == 0 ? 1 : (xm3 == 1 ? 0 : 2);         // B window for rows (x+1, x, x-1)
+        const uint64_t a = adesc0 + ((A_OFF + (x & 1) * NPART * ROW) >> 4);
+        const uint64_t bw = bdesc0 + ((o * C * 16) >> 4);
+        mma36_row(tmem + (uint32_t)((x % NRING) * 3 * C), a, a + (ROW >> 4), a + ((2 * ROW) >> 4), bw,
+                  bw + ((6 * TILE) >> 4), bw + ((12 * TILE) >> 4), acc_full(x));
+        __syncwarp();
+      }
+    }
+  } else {
+  uint32_t ph_acc = 0, ph_stg = 0;
+#ifdef CT_TL
+  int ctl_n = 0;
+#endif
   float xin[HC], vals[HC];
+  float bv[HC], mv[HC], rv[HC];   // bias of this thread's channels; next row's mask / residual
+#pragma unroll
+  for (int i = 0; i < HC; ++i) bv[i] = P.bias ? __ldg(P.bias + c0 + i) : 0.f;
   for (long long qq = q0; qq < q1;) {
     const int s = (int)(qq / range);
     const long long end = min(q1, (long long)(s + 1) * range);
@@ -230,11 +325,29 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
     const bool lane_valid = l >= 1 && l < 1 + S && in_img;
     const float *xb = P.x + ((size_t)b * C + c0) * plane + col;
     auto load_row = [&](int row) {
+      if constexpr (!TX) {
 #pragma unroll
-      for (int i = 0; i < HC; ++i) xin[i] = 0.f;
-      if (in_img && row < Bn) {
+        for (int i = 0; i < HC; ++i) xin[i] = 0.f;
+        if (in_img && row < Bn) {
 #pragma unroll
-        for (int i = 0; i < HC; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
+          for (int i = 0; i < HC; ++i) xin[i] = __ldg(xb + (size_t)i * plane + (size_t)row * P.W);
+        }
+      }
+    };
+    // TX: this thread's 16 channels of staged row `row` (box of its image)
+    const int kbox = in_img ? b - max(s * S - 1, 0) / (P.W + 1) : -1;
+    // lane l of box k sits at column l + ((c_k) & 3), c_k = the box's lane-0 column
+    const int kcol = (s * S - 1) - (max(s * S - 1, 0) / (P.W + 1) + max(kbox, 0)) * (P.W + 1);
+    const int koff = l + (kcol & 3);
+    auto stage_row = [&](int row) {
+      if constexpr (TX) {
+        if (lane == 0) mbar_wait(stg_full(row), (ph_stg >> (row & 1)) & 1);
+        ph_stg ^= 1u << (row & 1);
+        __syncwarp();
+        const float *src = reinterpret_cast<const float *>(smem + STG_OFF + (row & 1) * STG_SLOT + max(kbox, 0) * BOX) +
+                           c0 * BOXW + koff;
+#pragma unroll
+        for (int i = 0; i < HC; ++i) xin[i] = kbox >= 0 ? src[i * BOXW] : 0.f;
       }
     };
     // this thread's 16 channels of an input row -> three bf16 parts in the
@@ -261,36 +374,31 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
     };
     // Input row x's products go to TMEM ring x mod 4 (three 32-column slots:
     // output rows mod 3); output row d is the sum of the slots d mod 3 of the
-    // rings of input rows d-1, d, d+1.  Step r issues MMA(r+1) first -- its
-    // ring last held row r-3, drained a step earlier -- and only then waits
-    // for MMA(r), so the tensor pipe always has the next row queued while
-    // the threads drain row r-1, split row r+2 and store row r-1.
+    // rings of input rows d-1, d, d+1.  The issuer warp runs MMA(r+1) as soon
+    // as row r+1 is split and row r-2 drained (ring (r+1) mod 4 last held row
+    // r-3), so the tensor pipe has the next row queued while the workers wait
+    // for MMA(r), drain row r-1, split row r+2 and store row r-1.
+    // mask / residual values of output row `row` for the epilogue (one row ahead)
+    auto load_epi = [&](int row) {
+      if (!(P.mask || P.resid) || !(row >= R0 && row < R1 && lane_valid)) return;
+      const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)row * P.W + col;
+#pragma unroll
+      for (int i = 0; i < HC; ++i) {
+        if (P.mask) mv[i] = __ldg(P.mask + o0 + (size_t)i * plane);
+        if (P.resid) rv[i] = __ldg(P.resid + o0 + (size_t)i * plane);
+      }
+    };
     load_row(A);                       // split in the first iteration (r = A-2)
+    load_epi(R0);
     int tm3 = ((A - 3) % 3 + 3) % 3;   // slot of row r-1 at t = A-2
     for (int r = A - 2; r <= Bn; ++r) {
+#ifdef CT_TL
+      if (blockIdx.x == 0 && threadIdx.x == 0 && ctl_n < 4096) g_ctl[ctl_n][0] = r;
+#endif
+      CTL(1);
       const int d = r - 1, slot = tm3;
       tm3 = tm3 == 2 ? 0 : tm3 + 1;
-      // ---- 1. issue MMA(r+1): its input row was split into A buffer (r+1)&1
-      //         in the previous step (barrier: every warp's split and drain of
-      //         that step are done)
-      const int rn = r + 1;
-      if (rn >= A && rn < Bn) {
-        const int q = rn & 1;
-        tc_fence_before();
-        __syncthreads();
-        if (warp == 0) {
-          tc_fence_after();
-          const int rot = slot == 0 ? 2 : slot - 1;              // (r+1) mod 3
-          const int o = rot == 0 ? 1 : (rot == 1 ? 0 : 2);       // B window for rows (r+2, r+1, r)
-          const uint64_t a = adesc0 + ((A_OFF + q * NPART * ROW) >> 4);
-          const uint64_t bw = bdesc0 + ((o * C * 16) >> 4);
-          mma36_row(tmem + (uint32_t)((rn % NRING) * 3 * C), a, a + (ROW >> 4), a + ((2 * ROW) >> 4), bw,
-                    bw + ((6 * TILE) >> 4), bw + ((12 * TILE) >> 4), acc_full(rn));
-          __syncwarp();
-        }
-      } else if (r == A - 2) {
-        __syncthreads();               // segment start: the previous segment's buffers are free
-      }
+      CTL(2);
       // ---- 2. MMA(r) done (and every earlier MMA; MMA(r+1) may still run)
       if (r >= A && r < Bn) {
         if (lane == 0) mbar_wait(acc_full(r), (ph_acc >> (r & 1)) & 1);
@@ -301,6 +409,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       // ---- 3. finished output row d -> registers: slots d mod 3 of the rings
       //         of input rows d-1, d, d+1 (a row outside [A, Bn) is zero
       //         padding: its ring holds an older row)
+      CTL(3);
       const bool drain = d >= A && d < Bn;
       if (drain) {
 #pragma unroll
@@ -317,23 +426,41 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       }
       // ---- 4. input row r+2 -> the three bf16 A planes of buffer (r+2)&1
       //         (last read by MMA(r), retired in step 2)
-      if (r + 2 >= A && r + 2 < Bn) split_row(r + 2);
-      // ---- 5. epilogue of row d (overlaps MMA(r+1)), 6. prefetch the row after
-      if (drain && d >= R0 && d < R1 && lane_valid) {
+      CTL(4);
+      if (r + 2 >= A && r + 2 < Bn) {
+        stage_row(r + 2);
+        split_row(r + 2);
+        // row r+2 split, row r-1 drained (the last reader of ring (r+2) mod 4)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ready(r + 2));
+      }
+      CTL(5);
+      // ---- 5. prefetch input row r+3 (split next step: a whole step of
+      //         latency cover -- every split's proxy fence waits for the
+      //         loads outstanding at that point, so they must be a step old)
+      if (r + 2 >= A && r + 2 < Bn) load_row(r + 3);
+      // ---- 6. epilogue of row d (overlaps MMA(r+1)); its mask / residual
+      //         values were loaded a step earlier; then those of row d+1
+      const bool store_d = drain && d >= R0 && d < R1 && lane_valid;
+      if (store_d) {
         const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
 #pragma unroll
         for (int i = 0; i < HC; ++i) {
-          const size_t idx = o0 + (size_t)i * plane;
-          float y = vals[i] + (P.bias ? __ldg(P.bias + c0 + i) : 0.f);
-          if (P.mask) y = __ldg(P.mask + idx) > 0.f ? y : 0.f;
-          if (P.resid) y += __ldg(P.resid + idx);
+          float y = vals[i] + bv[i];
+          if (P.mask) y = mv[i] > 0.f ? y : 0.f;
+          if (P.resid) y += rv[i];
           if (P.relu) y = fmaxf(y, 0.f);
-          P.out[idx] = y;
+          P.out[o0 + (size_t)i * plane] = y;
         }
       }
-      if (r + 2 >= A && r + 2 < Bn) load_row(r + 3);
+      load_epi(d + 1);
+#ifdef CT_TL
+      ++ctl_n;
+#endif
     }
   }
+  }   // workers
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -343,6 +470,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
 }
 
 }  // namespace tct
+#ifdef CT_TL
+extern "C" int ht_debug_conv_timeline(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, tct::g_ctl, sizeof(long long) * 4096 * 6);
+}
+#endif
 
 // x, out, mask, resid: (B, 32, H, W) fp32; w: (32, 32, 3, 3) fp32 OIHW.
 int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
@@ -350,7 +482,8 @@ int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *
   using namespace tct;
   static bool attr = false;
   if (!attr) {
-    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LDG));
+    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TMA));
     attr = true;
   }
   int dev = 0, n_sm = 148;
@@ -366,7 +499,23 @@ int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *
   if (grid < 1) grid = 1;
   p.chunk = (total + grid - 1) / grid;
   grid = (total + p.chunk - 1) / p.chunk;
-  conv_tc_kernel<<<(unsigned)grid, NTHR, SMEM, st>>>(p);
+  // TMA-staged rows need 16-B row strides and strips spanning <= 2 images
+  if (W % 4 == 0 && W + 1 >= M) {
+    auto enc = tensor_map_encoder();
+    HT_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t row = (cuuint64_t)W * 4, planeb = row * H;
+    cuuint64_t dims[4] = {(cuuint64_t)W, (cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[3] = {planeb, row, planeb * C};
+    cuuint32_t box[4] = {(cuuint32_t)BOXW, (cuuint32_t)C, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = enc(&p.tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HT_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    conv_tc_kernel<true><<<(unsigned)grid, NTHR, SMEM_TMA, st>>>(p);
+  } else {
+    conv_tc_kernel<false><<<(unsigned)grid, NTHR, SMEM_LDG, st>>>(p);
+  }
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
