@@ -15,8 +15,10 @@ buf = (C.c_longlong * (4096 * 6))()
 lib.ht_debug_conv_timeline(buf)
 a = np.frombuffer(buf, dtype=np.int64).reshape(4096, 6)
 a = a[a[:, 1] > 0][10:-10]
+stg = a[:, 0] - a[:, 4]
 per = np.diff(a[:, 1])
 print("steps", len(a), "period median", int(np.median(per)))
 for k, name in ((2, "barrier+issue"), (3, "wait MMA(r)"), (4, "drain"), (5, "split")):
     print(f"  {name:14s} {int(np.median(a[:, k] - a[:, k - 1]))}")
+print(f"  {'(stage wait+LDS)':14s} {int(np.median(stg))}")
 print(f"  {'store+load':14s} {int(np.median(a[1:, 1] - a[:-1, 5]))}")

@@ -72,6 +72,19 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16 &p0, __nv_bfloat16
   p1 = __float2bfloat16_rn(r1);
   p2 = __float2bfloat16_rn(r1 - __bfloat162float(p1));
 }
+// split3 of a pair with packed conversions (one cvt.rn.bf16x2 per part: half
+// the conversion-pipe instructions); p_i = {part i of x (low), of y (high)}
+__device__ __forceinline__ void split3x2(float x, float y, uint32_t &p0, uint32_t &p1, uint32_t &p2) {
+  auto cvt2 = [](float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t *>(&v);
+  };
+  p0 = cvt2(x, y);
+  const float rx = x - __uint_as_float(p0 << 16), ry = y - __uint_as_float(p0 & 0xFFFF0000u);
+  p1 = cvt2(rx, ry);
+  const float sx = rx - __uint_as_float(p1 << 16), sy = ry - __uint_as_float(p1 & 0xFFFF0000u);
+  p2 = cvt2(sx, sy);
+}
 __device__ __forceinline__ uint32_t pack_bf2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
 }
@@ -311,6 +324,9 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
 #endif
   float xin[HC], vals[HC];
   float bv[HC], mv[HC], rv[HC];   // bias of this thread's channels; next row's mask / residual
+  constexpr size_t NO_ROW = ~(size_t)0;
+  float pend[HC];                 // output row awaiting its stores
+  size_t pend_o0 = NO_ROW;
 #pragma unroll
   for (int i = 0; i < HC; ++i) bv[i] = P.bias ? __ldg(P.bias + c0 + i) : 0.f;
   for (long long qq = q0; qq < q1;) {
@@ -359,12 +375,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
         uint32_t w[3][4];
 #pragma unroll
         for (int k2 = 0; k2 < 4; ++k2) {
-          __nv_bfloat16 a0, a1, a2, c0, c1, c2;
-          split3(xin[8 * g + 2 * k2], a0, a1, a2);
-          split3(xin[8 * g + 2 * k2 + 1], c0, c1, c2);
-          w[0][k2] = pack_bf2(a0, c0);
-          w[1][k2] = pack_bf2(a1, c1);
-          w[2][k2] = pack_bf2(a2, c2);
+          split3x2(xin[8 * g + 2 * k2], xin[8 * g + 2 * k2 + 1], w[0][k2], w[1][k2], w[2][k2]);
         }
 #pragma unroll
         for (int pp = 0; pp < 3; ++pp)
@@ -386,6 +397,14 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       for (int i = 0; i < HC; ++i) {
         if (P.mask) mv[i] = __ldg(P.mask + o0 + (size_t)i * plane);
         if (P.resid) rv[i] = __ldg(P.resid + o0 + (size_t)i * plane);
+      }
+    };
+    // deferred stores of the previous output row
+    auto flush = [&]() {
+      if (pend_o0 != NO_ROW) {
+#pragma unroll
+        for (int i = 0; i < HC; ++i) P.out[pend_o0 + (size_t)i * plane] = pend[i];
+        pend_o0 = NO_ROW;
       }
     };
     load_row(A);                       // split in the first iteration (r = A-2)
@@ -429,29 +448,35 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       CTL(4);
       if (r + 2 >= A && r + 2 < Bn) {
         stage_row(r + 2);
+#ifdef CT_TL
+        if (blockIdx.x == 0 && threadIdx.x == 0 && ctl_n < 4096) g_ctl[ctl_n][0] = clock64();
+#endif
         split_row(r + 2);
         // row r+2 split, row r-1 drained (the last reader of ring (r+2) mod 4)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ready(r + 2));
       }
+      flush();
       CTL(5);
       // ---- 5. prefetch input row r+3 (split next step: a whole step of
       //         latency cover -- every split's proxy fence waits for the
       //         loads outstanding at that point, so they must be a step old)
       if (r + 2 >= A && r + 2 < Bn) load_row(r + 3);
       // ---- 6. epilogue of row d (overlaps MMA(r+1)); its mask / residual
-      //         values were loaded a step earlier; then those of row d+1
+      //         values were loaded a step earlier; then those of row d+1.
+      //         Its stores go out after the next step's split, so that
+      //         split's proxy fence finds them a step old.
       const bool store_d = drain && d >= R0 && d < R1 && lane_valid;
       if (store_d) {
-        const size_t o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
+        pend_o0 = ((size_t)b * C + c0) * plane + (size_t)d * P.W + col;
 #pragma unroll
         for (int i = 0; i < HC; ++i) {
           float y = vals[i] + bv[i];
           if (P.mask) y = mv[i] > 0.f ? y : 0.f;
           if (P.resid) y += rv[i];
           if (P.relu) y = fmaxf(y, 0.f);
-          P.out[o0 + (size_t)i * plane] = y;
+          pend[i] = y;
         }
       }
       load_epi(d + 1);
@@ -459,6 +484,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc_kernel(const __grid_constant_
       ++ctl_n;
 #endif
     }
+    flush();
   }
   }   // workers
   tc_fence_before();
