@@ -130,13 +130,26 @@ class PolicyNetwork:
             self._dev = torch.device("cuda", torch.cuda.current_device())
         return self._dev
 
+    def _host_matches_upload(self):
+        """Host .value arrays still equal the last uploaded / pulled values
+        (checked per tensor against views of the snapshot: no concatenation,
+        stops at the first difference)."""
+        at = 0
+        up = self._uploaded
+        for p in self._params:
+            n = p.value.size
+            if not np.array_equal(p.value.ravel(), up[at:at + n]):
+                return False
+            at += n
+        return True
+
     def sync(self, force=False):
         """Upload + repack if the host parameter values changed."""
         torch = _torch()
-        flat = self.flat_values()
         if (not force and self._flat is not None and self._uploaded is not None
-                and np.array_equal(flat, self._uploaded)):
+                and self._host_matches_upload()):
             return
+        flat = self.flat_values()
         dev = self.device
         with torch.cuda.device(dev):
             if self._flat is None:
@@ -160,11 +173,17 @@ class PolicyNetwork:
         return self._packed
 
     def pull_from_device(self):
-        """Device params (after a device-side update) -> host arrays."""
-        flat = self._flat.detach().cpu().numpy().copy()
+        """Device params (after a device-side update) -> host arrays (through
+        a pinned staging buffer)."""
+        torch = _torch()
+        self._repack()
+        if getattr(self, "_pin", None) is None or self._pin.numel() != self._flat.numel():
+            self._pin = torch.empty(self._flat.numel(), dtype=torch.float64, pin_memory=True)
+        self._pin.copy_(self._flat, non_blocking=True)
+        torch.cuda.current_stream(self._flat.device).synchronize()
+        flat = self._pin.numpy().copy()
         self.set_flat_values(flat)
         self._uploaded = flat
-        self._repack()
 
     # ------------------------------------------------------------------ compute
     def forward(self, x):

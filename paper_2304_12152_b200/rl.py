@@ -469,7 +469,8 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     bin_gap = float(st[1] / (bs * size * size))
     l_as = float(st[2] / (cfg.anisotropy_batch_size or bs)) if run_aniso else math.nan
     lr = cosine_lr(t, cfg.iterations, cfg.lr_start, cfg.lr_end)
-    net.sync()
+    # (the device parameters are current: forward_device synced them and no
+    # host code of this step changes them)
     adam.step_device(net._flat, grad, lr)
     net.pull_from_device()
     net._last_grad = grad
