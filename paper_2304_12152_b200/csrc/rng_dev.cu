@@ -73,31 +73,54 @@ void jump_host(uint64_t s[4], uint64_t n) {
     if (n & 1) matvec_host(t[k], s);
 }
 
-static const Mat *device_tables() {
+// Device form of the jump matrices: per level, 64 nibble tables
+// N[c][v] = XOR of the columns 4c + i for the set bits i of v, so a product
+// is 64 lookups instead of 256 masked column XORs.
+struct NibMat {
+  ulonglong4 t[64][16];
+};
+
+static const NibMat *device_tables() {
   static std::mutex mu;
-  static const Mat *per_dev[64] = {nullptr};
+  static const NibMat *per_dev[64] = {nullptr};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   if (!per_dev[dev]) {
-    Mat *d = nullptr;
-    if (cudaMalloc(&d, sizeof(Mat) * LEVELS) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, tables().data(), sizeof(Mat) * LEVELS, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    std::vector<NibMat> h(LEVELS);
+    const auto &t = tables();
+    for (int k = 0; k < LEVELS; ++k)
+      for (int c = 0; c < 64; ++c)
+        for (int v = 0; v < 16; ++v) {
+          uint64_t o[4] = {0, 0, 0, 0};
+          for (int i = 0; i < 4; ++i)
+            if ((v >> i) & 1)
+              for (int w = 0; w < 4; ++w) o[w] ^= t[k].col[4 * c + i][w];
+          h[k].t[c][v] = make_ulonglong4(o[0], o[1], o[2], o[3]);
+        }
+    NibMat *d = nullptr;
+    if (cudaMalloc(&d, sizeof(NibMat) * LEVELS) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h.data(), sizeof(NibMat) * LEVELS, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
     per_dev[dev] = d;
   }
   return per_dev[dev];
 }
 
-__device__ __forceinline__ void jump_dev(const Mat *__restrict__ J, uint64_t s[4], uint64_t n) {
+__device__ __forceinline__ void jump_dev(const NibMat *__restrict__ J, uint64_t s[4], uint64_t n) {
   for (int k = 0; k < LEVELS && n; ++k, n >>= 1) {
     if (!(n & 1)) continue;
     uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-    const ulonglong2 *c = reinterpret_cast<const ulonglong2 *>(J[k].col);
-#pragma unroll 4
-    for (int j = 0; j < 256; ++j) {
-      const ulonglong2 a = __ldg(c + 2 * j), b = __ldg(c + 2 * j + 1);
-      const uint64_t m = 0ull - ((s[j >> 6] >> (j & 63)) & 1ull);
-      o0 ^= a.x & m; o1 ^= a.y & m; o2 ^= b.x & m; o3 ^= b.y & m;
+    const ulonglong2 *base = reinterpret_cast<const ulonglong2 *>(J[k].t);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint64_t sw = s[w];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int c = w * 16 + q;
+        const int v = (int)((sw >> (4 * q)) & 15u);
+        const ulonglong2 a = __ldg(base + 2 * (c * 16 + v)), b = __ldg(base + 2 * (c * 16 + v) + 1);
+        o0 ^= a.x; o1 ^= a.y; o2 ^= b.x; o3 ^= b.y;
+      }
     }
     s[0] = o0; s[1] = o1; s[2] = o2; s[3] = o3;
   }
@@ -111,7 +134,7 @@ __device__ __forceinline__ uint64_t next_dev(uint64_t s[4]) {
 }
 __device__ __forceinline__ double unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
 
-constexpr int PAIRS_PER_THREAD = 128;
+constexpr int PAIRS_PER_THREAD = 16;
 
 // Noise maps of n gaussians each (n gaussians = ceil(n/2) Box-Muller pairs,
 // pair i consuming draws 2i, 2i+1 of its map's stream), map m starting from
@@ -124,7 +147,7 @@ struct MapStarts {
 };
 
 template <typename T>
-__global__ void gaussian_maps_kernel(const __grid_constant__ MapStarts st, int64_t n, const Mat *__restrict__ J,
+__global__ void gaussian_maps_kernel(const __grid_constant__ MapStarts st, int64_t n, const NibMat *__restrict__ J,
                                      T *__restrict__ out) {
   const int64_t npairs = (n + 1) / 2;
   const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * PAIRS_PER_THREAD;
@@ -150,7 +173,7 @@ template <typename T>
 static int launch_maps(const uint64_t *states, int n_maps, int64_t n, T *out, cudaStream_t st) {
   HT_REQUIRE(n_maps >= 0 && n >= 0, "counts must be non-negative");
   if (n_maps == 0 || n == 0) return HT_OK;
-  const Mat *J = device_tables();
+  const NibMat *J = device_tables();
   HT_REQUIRE(J != nullptr, "could not upload RNG jump tables");
   const int threads = 128;
   const int64_t units = ((n + 1) / 2 + PAIRS_PER_THREAD - 1) / PAIRS_PER_THREAD;
@@ -169,10 +192,10 @@ static int launch_maps(const uint64_t *states, int n_maps, int64_t n, T *out, cu
   return HT_OK;
 }
 
-constexpr int DRAWS_PER_THREAD = 256;
+constexpr int DRAWS_PER_THREAD = 32;
 
 template <typename T>
-__global__ void uniforms_kernel(ulonglong4 start, int64_t n, const Mat *__restrict__ J, T *__restrict__ out) {
+__global__ void uniforms_kernel(ulonglong4 start, int64_t n, const NibMat *__restrict__ J, T *__restrict__ out) {
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * DRAWS_PER_THREAD;
   if (i0 >= n) return;
   uint64_t s[4] = {start.x, start.y, start.z, start.w};
@@ -185,7 +208,7 @@ template <typename T>
 static int launch_uniforms(uint64_t state[4], int64_t n, T *out, cudaStream_t st) {
   HT_REQUIRE(n >= 0, "n must be non-negative");
   if (n == 0) return HT_OK;
-  const Mat *J = device_tables();
+  const NibMat *J = device_tables();
   HT_REQUIRE(J != nullptr, "could not upload RNG jump tables");
   const ulonglong4 s0 = make_ulonglong4(state[0], state[1], state[2], state[3]);
   const int threads = 128;
