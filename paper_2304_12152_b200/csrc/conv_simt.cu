@@ -106,23 +106,40 @@ conv3x3_fwd_kernel(const float *__restrict__ x, int H, int W,
 // accumulates in fp32 registers, then atomically adds into the fp64 grads.
 constexpr int WT_X = 32, WT_Y = 8;
 
+// Generic weight / bias gradient (the convs other than 32 -> 32: conv_in's
+// 2 -> C, conv_out's C -> 1, and the small presets).  Thread (ci, tap, k)
+// accumulates the KS output channels co = k*KS .. of one (ci, tap) over a tile
+// of WT_Y x WT_X pixels; dout is staged pixel-major with a padded row so the
+// coalesced (pixel-fastest) loads and the per-pixel broadcast reads are both
+// conflict-free.
 template <int CIN, int COUT>
-__global__ void __launch_bounds__(CIN * 9 < 64 ? 64 : CIN * 9)
+struct WgSimt {
+  static constexpr int KS = COUT >= 16 ? 2 : COUT;          // output channels per thread
+  static constexpr int NK = COUT / KS;
+  static constexpr int ACTIVE = CIN * 9 * NK;
+  static constexpr int NT = ACTIVE < 64 ? 64 : (ACTIVE + 31) / 32 * 32;
+  static constexpr int DP = COUT + 1;                        // padded dout row
+};
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(WgSimt<CIN, COUT>::NT)
 conv3x3_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dout,
                      int B, int H, int W, int tiles_per_cta,
                      double *__restrict__ dw, double *__restrict__ db) {
-  constexpr int NT = CIN * 9 < 64 ? 64 : CIN * 9;
-  constexpr int TXP = WT_X + 2, TYP = WT_Y + 2;
+  using L = WgSimt<CIN, COUT>;
+  constexpr int NT = L::NT, KS = L::KS, DP = L::DP;
+  constexpr int TXP = WT_X + 2, TYP = WT_Y + 2, NP = WT_Y * WT_X;
   extern __shared__ float smem[];
   float *xs = smem;                                  // [CIN][TYP][TXP]
-  float *ds = smem + CIN * TYP * TXP;                // [WT_Y*WT_X][COUT]
+  float *ds = smem + CIN * TYP * TXP;                // [NP][DP]
   const int tid = threadIdx.x;
-  const bool active = tid < CIN * 9;
-  const int ci = tid / 9, tap = tid % 9, ky = tap / 3, kx = tap % 3;
-  float acc[COUT];
+  const bool active = tid < L::ACTIVE;
+  const int ct = tid / L::NK, k = tid % L::NK;      // (ci, tap), output-channel group
+  const int ci = ct / 9, tap = ct % 9, ky = tap / 3, kx = tap % 3;
+  float acc[KS];
   float bacc = 0.f;
 #pragma unroll
-  for (int j = 0; j < COUT; ++j) acc[j] = 0.f;
+  for (int j = 0; j < KS; ++j) acc[j] = 0.f;
   const int tx_n = (W + WT_X - 1) / WT_X, ty_n = (H + WT_Y - 1) / WT_Y;
   const long total_tiles = (long)B * tx_n * ty_n;
   const size_t plane = (size_t)H * W;
@@ -142,32 +159,32 @@ conv3x3_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dout
         v = x[((size_t)b * CIN + c) * plane + (size_t)gy * W + gx];
       xs[i] = v;
     }
-    for (int i = tid; i < WT_Y * WT_X * COUT; i += NT) {
-      const int co = i % COUT, p = i / COUT;
+    for (int i = tid; i < NP * COUT; i += NT) {
+      const int p = i % NP, co = i / NP;             // pixel fastest: coalesced
       const int gy = y0 + p / WT_X, gx = x0 + p % WT_X;
       float v = 0.f;
       if (gy < H && gx < W) v = dout[((size_t)b * COUT + co) * plane + (size_t)gy * W + gx];
-      ds[i] = v;
+      ds[p * DP + co] = v;
     }
     __syncthreads();
     if (active) {
       const float *xr = xs + ci * TYP * TXP + ky * TXP + kx;
-#pragma unroll 2
-      for (int p = 0; p < WT_Y * WT_X; ++p) {
+#pragma unroll 4
+      for (int p = 0; p < NP; ++p) {
         const float xv = xr[(p / WT_X) * TXP + (p % WT_X)];
-        const float *dr = ds + p * COUT;
+        const float *dr = ds + p * DP + k * KS;
 #pragma unroll
-        for (int co = 0; co < COUT; ++co) acc[co] = fmaf(dr[co], xv, acc[co]);
+        for (int j = 0; j < KS; ++j) acc[j] = fmaf(dr[j], xv, acc[j]);
       }
     }
     if (tid < COUT) {
-      for (int p = 0; p < WT_Y * WT_X; ++p) bacc += ds[p * COUT + tid];
+      for (int p = 0; p < NP; ++p) bacc += ds[p * DP + tid];
     }
   }
   if (active) {
 #pragma unroll
-    for (int co = 0; co < COUT; ++co)
-      atomicAdd(&dw[((size_t)co * CIN + ci) * 9 + tap], (double)acc[co]);
+    for (int j = 0; j < KS; ++j)
+      atomicAdd(&dw[((size_t)(k * KS + j) * CIN + ci) * 9 + tap], (double)acc[j]);
   }
   if (tid < COUT) atomicAdd(&db[tid], (double)bacc);
 }
@@ -349,8 +366,8 @@ static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, do
     HT_CHECK_LAUNCH();
     return HT_OK;
   }
-  constexpr int NT = CIN * 9 < 64 ? 64 : CIN * 9;
-  const size_t smem = sizeof(float) * ((size_t)CIN * (WT_Y + 2) * (WT_X + 2) + WT_Y * WT_X * COUT);
+  constexpr int NT = WgSimt<CIN, COUT>::NT;
+  const size_t smem = sizeof(float) * ((size_t)CIN * (WT_Y + 2) * (WT_X + 2) + WT_Y * WT_X * WgSimt<CIN, COUT>::DP);
   static bool attr_set = false;
   if (!attr_set) {
     HT_CUDA(cudaFuncSetAttribute(conv3x3_wgrad_kernel<CIN, COUT>,
