@@ -181,8 +181,10 @@ class PolicyNetwork:
             self._pin = torch.empty(self._flat.numel(), dtype=torch.float64, pin_memory=True)
         self._pin.copy_(self._flat, non_blocking=True)
         torch.cuda.current_stream(self._flat.device).synchronize()
-        flat = self._pin.numpy().copy()
+        flat = self._pin.numpy()
         self.set_flat_values(flat)
+        # the pinned buffer doubles as the snapshot sync() compares against:
+        # it is only rewritten by the next pull, after which it matches again
         self._uploaded = flat
 
     # ------------------------------------------------------------------ compute
