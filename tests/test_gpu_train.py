@@ -238,3 +238,40 @@ def test_train_step_prefetch_is_transparent():
             for key in ("reward", "l_as", "bin_gap"):
                 assert abs(ra[key] - rb[key]) <= 1e-12 * max(1.0, abs(rb[key])), (kw, key)
             assert ra["lr"] == rb["lr"] and ra["iteration"] == rb["iteration"]
+
+
+def test_host_parameter_edits_between_steps_reach_the_device():
+    """The device copy of the parameters follows the host Parameter arrays
+    (nn.py's API surface): after a train_step pulled the Adam update back,
+    an in-place edit of one tensor's .value -- and a whole-array replace of
+    another's contents -- must be seen by the next forward, which must then
+    equal the oracle forward with the edited parameters; an untouched net
+    must not re-upload."""
+    import torch
+
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    g = golden("train.npz")
+    cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
+                         anisotropy_batch_size=2, hvs_model="gaussian")
+    net = PolicyNetwork(8, 2)
+    adam = Adam(net.params())
+    rng = Rng(cfg.seed)
+    net.init_params(rng)
+    rl.train_step(net, adam, list(g["mini_ds"]), cfg, rng, 0)
+    r = Rng(9)
+    x = np.stack((r.uniforms(20 * 22).reshape(20, 22), r.gaussians(20 * 22).reshape(20, 22)))[None]
+    x = x.astype(np.float32).astype(np.float64)
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    uploaded = net._uploaded
+    p0 = net.forward_device(xd).double().cpu().numpy()
+    assert net._uploaded is uploaded                      # nothing changed: no re-upload
+    ps = net.params()
+    ps[0].value[0, 1, 2, 2] += 0.25                        # in place, one element
+    ps[-2].value[...] = ps[-2].value * 0.5                 # whole tensor
+    p1 = net.forward_device(xd).double().cpu().numpy()
+    ref = O.policy_forward([q.value for q in ps], x)
+    assert np.max(np.abs(p1 - ref[:, 0])) < 2e-5
+    assert np.max(np.abs(p1 - p0)) > 1e-4
