@@ -144,11 +144,12 @@ class PolicyNetwork:
         return True
 
     def sync(self, force=False):
-        """Upload + repack if the host parameter values changed."""
+        """Upload + repack if the host parameter values changed; True if it
+        uploaded."""
         torch = _torch()
         if (not force and self._flat is not None and self._uploaded is not None
                 and self._host_matches_upload()):
-            return
+            return False
         flat = self.flat_values()
         dev = self.device
         with torch.cuda.device(dev):
@@ -159,6 +160,7 @@ class PolicyNetwork:
             self._flat.copy_(torch.from_numpy(flat))
             self._repack()
         self._uploaded = flat
+        return True
 
     def _repack(self):
         _lib.call("ht_pack_params", _lib.ptr(self._flat), self.channels, self.blocks,
@@ -175,16 +177,26 @@ class PolicyNetwork:
     def pull_from_device(self):
         """Device params (after a device-side update) -> host arrays (through
         a pinned staging buffer)."""
+        self._pull_start()
+        self._pull_finish()
+
+    def _pull_start(self):
+        """Repack the updated device parameters and start their copy to the
+        pinned staging buffer (stream-ordered, no wait)."""
         torch = _torch()
         self._repack()
         if getattr(self, "_pin", None) is None or self._pin.numel() != self._flat.numel():
             self._pin = torch.empty(self._flat.numel(), dtype=torch.float64, pin_memory=True)
         self._pin.copy_(self._flat, non_blocking=True)
-        torch.cuda.current_stream(self._flat.device).synchronize()
-        flat = self._pin.numpy()
+        self._pin_done = torch.cuda.Event()
+        self._pin_done.record(torch.cuda.current_stream(self._flat.device))
+
+    def _pull_finish(self):
+        """Wait for the copy only (not for work queued after it) and update
+        the host arrays."""
+        self._pin_done.synchronize()
+        flat = self._pin.numpy().copy()   # (the next pull rewrites the pinned buffer early)
         self.set_flat_values(flat)
-        # the pinned buffer doubles as the snapshot sync() compares against:
-        # it is only rewritten by the next pull, after which it matches again
         self._uploaded = flat
 
     # ------------------------------------------------------------------ compute
@@ -201,7 +213,7 @@ class PolicyNetwork:
         p = self.forward_device(xd)
         return p.double().cpu().numpy()[:, None]
 
-    def forward_device(self, x, flag=None):
+    def forward_device(self, x, flag=None, _sync=True):
         """Training forward on a device tensor x (B, 2, H, W) float32 ->
         p (B, H, W) float32 device tensor; activations cached.  Raises
         FloatingPointError on non-finite logits (nn.py:147-148) -- or, with
@@ -210,7 +222,8 @@ class PolicyNetwork:
         later."""
         torch = _torch()
         _lib.require_cuda()
-        self.sync()
+        if _sync:
+            self.sync()
         if x.dim() != 4 or x.shape[1] != self.in_channels:
             raise ValueError("input must be (batch, 2, height, width)")
         B, _, H, W = x.shape

@@ -378,6 +378,26 @@ def _take_prepared(dataset, cfg, rng, dev, rank, world):
     return _prepare_step(dataset, cfg, rng, dev, rank, world)
 
 
+def _speculate_forward(net, dev):
+    """Queue the next step's forward (its prepared inputs, the parameters
+    Adam just produced) behind this step's work, so the GPU does not idle
+    while the host finishes this step and starts the next; the next step uses
+    it only if it takes the same prepared batch and uploads no parameters."""
+    torch = _torch()
+    prep = _next_step.get("prep")
+    if prep is None or not prep["inputs"]:
+        return
+    own = net._cache
+    ins = prep["inputs"]
+    x = ins[0] if len(ins) == 1 else torch.cat(ins)
+    flag = torch.zeros(max(prep["nm"] + prep["ng"], 1), dtype=torch.int32, device=dev)
+    # (no host-parameter check: this step changed none; the device copy is
+    # Adam's update, which the pull now under way brings to the host)
+    p = net.forward_device(x.contiguous(), flag=flag, _sync=False)
+    _next_step["spec"] = {"prep": prep, "net": net, "p": p, "flag": flag, "cache": net._cache}
+    net._cache = own
+
+
 def _prefetch_next(dataset, cfg, rng, dev, rank, world):
     ahead = Rng(0)
     ahead.set_state_words(rng.state_words())
@@ -403,6 +423,7 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     bs = cfg.batch_size
     mcfg = cfg.metric_config()
     prep = _take_prepared(dataset, cfg, rng, dev, rank, world)
+    spec = _next_step.pop("spec", None)
     lo, nm, ng, ba = prep["lo"], prep["nm"], prep["ng"], prep["ba"]
     cd, ud, inputs, rng_at_fwd = prep["cd"], prep["ud"], prep["inputs"], prep["rng_at_fwd"]
     size = cfg.crop_size
@@ -416,8 +437,14 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     # parameters do not change in between); sample b's non-finite flag
     nonfinite = torch.zeros(max(nm + ng, 1), dtype=torch.int32, device=dev)
     if nm + ng:
-        x = inputs[0] if len(inputs) == 1 else torch.cat(inputs)
-        p_all = net.forward_device(x.contiguous(), flag=nonfinite)
+        # the previous step may already have run this forward (same prepared
+        # inputs, same parameters: nothing was uploaded since)
+        uploaded = net.sync()
+        if spec is not None and spec["prep"] is prep and spec["net"] is net and not uploaded:
+            p_all, nonfinite, net._cache = spec["p"], spec["flag"], spec["cache"]
+        else:
+            x = inputs[0] if len(inputs) == 1 else torch.cat(inputs)
+            p_all = net.forward_device(x.contiguous(), flag=nonfinite, _sync=False)
     dps = []
     reinforce = cfg.estimator in ("reinforce", "reinforce_meanbaseline")
     if nm:
@@ -472,7 +499,10 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     # (the device parameters are current: forward_device synced them and no
     # host code of this step changes them)
     adam.step_device(net._flat, grad, lr)
-    net.pull_from_device()
+    net._pull_start()
+    if prefetch:
+        _speculate_forward(net, dev)
+    net._pull_finish()
     net._last_grad = grad
     return {"iteration": t, "reward": mean_reward, "l_as": l_as, "bin_gap": bin_gap, "lr": lr}
 
