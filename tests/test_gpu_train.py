@@ -200,11 +200,12 @@ def test_train_step_nonfinite_raises_before_update():
 
 def test_train_step_prefetch_is_transparent():
     """train_step prepares the next step's batch from a copy of the RNG
-    stream while the GPU works; with or without it, three steps draw the
-    same stream (RNG state bit for bit) and give the same parameters and
-    diagnostics (to the run-to-run noise of atomic sums), and a dataset
-    image replaced between steps (or an RNG moved by the caller) makes the
-    next step draw afresh."""
+    stream while the GPU works, and queues that batch's forward after Adam;
+    with or without it, three steps draw the same stream (RNG state bit for
+    bit) and give the same parameters and diagnostics (to the run-to-run
+    noise of atomic sums), and a dataset image replaced between steps (or an
+    RNG moved by the caller) makes the next step draw afresh, a weight edited
+    by the caller makes it recompute the forward."""
     from paper_2304_12152_b200 import rl
     from paper_2304_12152_b200.imagecore import Rng
     from paper_2304_12152_b200.nn import Adam, PolicyNetwork
@@ -212,7 +213,7 @@ def test_train_step_prefetch_is_transparent():
     cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
                          anisotropy_batch_size=2, hvs_model="gaussian")
 
-    def run(prefetch, swap=False, poke=False):
+    def run(prefetch, swap=False, poke=False, edit=False):
         ds = list(g["mini_ds"])
         net = PolicyNetwork(8, 2)
         adam = Adam(net.params())
@@ -224,12 +225,15 @@ def test_train_step_prefetch_is_transparent():
                 ds[0] = ds[0][::-1].copy()        # a different image in the same list
             if poke and t == 2:
                 rng.uniform()                      # the caller draws from the stream
+            if edit and t == 1:
+                net.params()[0].value[0, 0, 1, 1] += 1e-2   # the caller edits a weight (the
+                #                                    forward queued by step 0 must be dropped)
             rows.append(rl.train_step(net, adam, ds, cfg, rng, t, prefetch=prefetch))
         return net.flat_values(), rows, rng.state_words()
 
     # gradients are summed with fp64 atomics (order varies run to run: two
     # runs of the same path differ by ~1e-18); the draws must match exactly
-    for kw in ({}, {"swap": True}, {"poke": True}):
+    for kw in ({}, {"swap": True}, {"poke": True}, {"edit": True}):
         a = run(True, **kw)
         b = run(False, **kw)
         assert a[2] == b[2], kw
