@@ -36,7 +36,10 @@ def _run(impl, x, w, bias=None, mask=None, resid=None, relu=0):
 # (W % 4 == 0 and W + 1 >= 128 take the TMA-staged input path: strips that
 # straddle two images, box starts at every 16-B phase)
 @pytest.mark.parametrize("B,H,W", [(1, 5, 6), (2, 20, 24), (3, 40, 52), (1, 7, 300), (2, 130, 67),
-                                   (3, 9, 128), (3, 6, 132), (4, 5, 136), (2, 11, 256)])
+                                   (3, 9, 128), (3, 6, 132), (4, 5, 136), (2, 11, 256),
+                                   # many short segments per CTA (issuer / worker phase
+                                   # tracking across strips), single-row images
+                                   (8, 3, 128), (5, 2, 252), (4, 1, 128)])
 @pytest.mark.parametrize("mode", ["plain", "bias_relu", "mask", "resid"])
 def test_conv_tc_matches_reference(B, H, W, mode):
     r = Rng(B * 1000 + H * 10 + W)
