@@ -1,26 +1,36 @@
 """Benchmark of the halftoning hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
 
-Workload (config 2 of BASELINE.json, the largest single-GPU config the metric
-is quoted on): 64 seeded synthetic 512x512 contones (ramp + 8 Gaussian blobs
-+ 2 rectangles, 10% with step edges) with N(0,1) noise maps from the
-reference RNG; the reference's default policy CNN (C=32, 16 blocks, 296,833
-params) with seeded random-init weights (std 0.01).  One step = fused
-forward + sigmoid/threshold (K1) over the rank's 64 images.  Multi-GPU is
-weak scaling: every rank halftones its own 64-image batch (independent
-images, no collective on the data path).
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under `python -m torch.distributed.run --nproc-per-node N` (one rank per GPU,
+NCCL, rendezvous on 127.0.0.1); under torchrun it checks WORLD_SIZE == N.
 
-value  = device-resident throughput (inputs in HBM), CUDA events, max over ranks.
-e2e    = same metric through rl.HalftoneEngine (public API): pinned host
-         contone+noise -> H2D -> K1 -> D2H uint8 halftones, every step;
-         batches streamed two deep (submit/wait), wall clock.
-roofline = the dominant kernel (the 2-residual-block pass, 7 of 9 launches),
-         algorithmic FLOPs per launch / its mean CUDA-event duration, against
-         the measured sustained bf16/fp16 dense peak (MEASURED_PEAKS.json).
-cpu_baseline = the CPU oracle (NumPy port of the reference forward) on the
-         host's cores over a bounded sample of the same images.
+Headline workload = BASELINE config 2: 64 seeded synthetic 512x512 contones
+(ramp + 8 Gaussian blobs + 2 rectangles, 10% with step edges) with N(0,1)
+noise maps from the reference RNG; the reference's default policy CNN (C=32,
+16 blocks, 296,833 params) with seeded random-init weights (std 0.01).  One
+step = fused forward + sigmoid/threshold (K1) over the 64 images, sharded
+64/N per rank (strong scaling, no collective on the data path).
+
+value    = device-resident throughput (inputs in HBM), CUDA events on the
+           launch stream, max over ranks.
+e2e      = same metric through rl.HalftoneEngine (public API): pinned host
+           contone+noise -> H2D -> K1 -> D2H uint8 halftones, every step,
+           batches streamed two deep (submit/wait), max over ranks.
+roofline = the dominant kernel (the 2-residual-block pass, 7 of 9 launches):
+           algorithmic FLOPs per launch / its mean CUDA-event duration,
+           against the measured burst bf16/fp16 dense peak (MEASURED_PEAKS).
+cpu_baseline = the REAL reference (htlab installed under baseline/_ref:
+           PolicyNetwork.forward + p >= 0.5, nn.py:138-150, rl.py:310-311) on
+           all host cores, single-threaded BLAS per worker process, one
+           256x256 tile of a config-2 image per core (bounded sample).
+configs  = the other BASELINE configs, each with its own clocks: cfg1
+           latency, cfg3 flat-gray sweep incl. spectra, cfg4 print page in
+           row strips, cfg5 training step (data parallel at N > 1).
+
+--impl reference: the reference arm (rank 0 only; other ranks exit 0): the
+same htlab forward + threshold on the host cores, same metric / config.
 """
 
 import argparse
@@ -35,11 +45,14 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 FLOP_PER_PX = 2 * 9 * (2 * 32 + 2 * 16 * 32 * 32 + 32)   # 591,552
 FLOP_PER_PX_MIDPASS = 2 * 9 * 4 * 32 * 32               # 4 convs of 32->32 per pass
 MID_TAG = 20                                             # pass tag: no conv_in, 2 blocks, no conv_out
 METRIC = "halftone Mpixel/s (CNN inference+binarize) at 1/2/4/8 B200; % of roofline"
+B2, S2 = 64, 512                                         # BASELINE config 2
+REF_TILE = 256                                           # reference sample tile edge
 
 
 def load_peaks():
@@ -49,6 +62,13 @@ def load_peaks():
         return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
     except Exception:
         return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def headline_config(world):
+    return {"workload": f"BASELINE config 2: {B2} x {S2}x{S2} contones, policy CNN C=32 B=16",
+            "global_batch": B2, "image": [S2, S2],
+            "parallelism": f"images sharded {B2}/{world} per rank, {world} rank(s), no collective",
+            "l2": "inputs (134 MB) + pass buffers larger than L2 (126 MB)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -67,10 +87,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.15)          # first sample lands inside the region
         except FileNotFoundError:
             self.proc = None
         return self
@@ -108,108 +129,406 @@ def noise_seed(seed):
     return seed * 1_000_003
 
 
-def make_inputs(B, H, W, seed, device=None):
-    """Contones from the BASELINE generator; noise maps drawn in image order
-    from one reference-RNG stream (as B calls of rl.infer_halftone would),
-    on the GPU when `device` is given (the same stream the e2e engine draws)."""
+def make_inputs(lo, hi, H, W, seed, device):
+    """Images [lo, hi) of the config-2 batch: contones from the BASELINE
+    generator (image i uses seed (seed, i)); noise maps drawn in image order
+    from one reference-RNG stream (as B calls of rl.infer_halftone would), on
+    the GPU, starting at image lo (jump-ahead over the earlier maps)."""
     from paper_2304_12152_b200 import synth
-    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_device, gaussian_noise_map_f32
-    c = synth.config_batch(B, H, W, seed=seed, blobs=8, rects=2, step_frac=0.1)
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_device
+    c = np.stack([synth.contone(H, W, seed=noise_seed(seed) + i, blobs=8, rects=2,
+                                step_edge=i < round(0.1 * B2)) for i in range(lo, hi)])
     rng = Rng(noise_seed(seed))
-    if device is not None:
-        z = np.stack([gaussian_noise_map_device(rng, W, H, device=device).cpu().numpy()
-                      for _ in range(B)])
-    else:
-        z = np.stack([gaussian_noise_map_f32(rng, W, H) for _ in range(B)])
+    rng.jump(lo * 2 * ((H * W + 1) // 2))
+    z = np.stack([gaussian_noise_map_device(rng, W, H, device=device).cpu().numpy()
+                  for _ in range(lo, hi)])
     return c, z
 
 
-def make_net():
+def make_net(std=0.01):
     from paper_2304_12152_b200.imagecore import Rng
     from paper_2304_12152_b200.nn import PolicyNetwork
     net = PolicyNetwork(32, 16)
-    net.init_params(Rng(0), std=0.01)
+    net.init_params(Rng(0), std=std)
     return net
 
 
-# ------------------------------------------------------------------ CPU baseline
-def _cpu_init():
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
+def l2_flush(dev, buf=[]):
+    """Write 256 MB (> 126 MB L2) so the next kernel starts from cold L2."""
+    import torch
+    if not buf:
+        buf.append(torch.empty(64 << 20, dtype=torch.float32, device=dev))
+    buf[0].fill_(1.0)
 
 
-def _cpu_worker(args):
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    c, z = args
-    from oracle import htoracle as O
-    params = O.init_params(O.Rng(0), 32, 16, 2, 0.01)
+# ------------------------------------------------------------------ reference (CPU)
+def _ref_worker_init(ref_path):
+    # single-threaded BLAS is already in the environment this process was
+    # spawned with; the reference is imported from its install only
+    sys.path.insert(0, ref_path)
+    global _REF_NET
+    from htlab import nn as hnn
+    from htlab.imagecore import Rng as HRng
+    _REF_NET = hnn.PolicyNetwork()              # PRESET_PAPER: C=32, 16 blocks
+    _REF_NET.init_params(HRng(0), std=0.01)
+
+
+def _ref_task(job):
+    """One tile through the reference's own path: forward + threshold
+    (nn.py:138-150, rl.py:310-311)."""
+    c, z = job
     t0 = time.perf_counter()
-    O.halftone(params, c.astype(np.float64), z.astype(np.float64))
-    return c.size, time.perf_counter() - t0
+    p = _REF_NET.forward(np.stack((c, z))[None])[0, 0]
+    h = p >= 0.5
+    return c.size, time.perf_counter() - t0, int(h.sum())
 
 
-def cpu_sample(c, z, tile, cores):
-    """Oracle (NumPy port of nn.py:138-150 + rl.py:311) on `cores` worker
-    processes, one tile x tile crop of a distinct image each."""
-    import multiprocessing as mp
+def _port_worker_init(_):
+    global _REF_NET
+    from oracle import htoracle as O
+    _REF_NET = O.init_params(O.Rng(0), 32, 16, 2, 0.01)
+
+
+def _port_task(job):
+    from oracle import htoracle as O
+    c, z = job
+    t0 = time.perf_counter()
+    _, p = O.halftone(_REF_NET, c, z)
+    return c.size, time.perf_counter() - t0, int((p >= 0.5).sum())
+
+
+_ref_images = {}
+
+
+def ref_tiles(n, tile):
+    """n tiles (tile x tile, float64 copies of the fp32 inputs) of the
+    config-2 images: tile k is quadrant k % 4 of image k // 4 (images in
+    batch order).  Noise maps come from the reference's own Rng stream (its
+    gaussian_noise_map, imagecore.py:155-159) when the reference is
+    installed, else the oracle port's (bit-identical, pinned by tests)."""
+    from paper_2304_12152_b200 import synth
+    if os.path.isdir(os.path.join(REF_PATH, "htlab")):
+        sys.path.insert(0, REF_PATH)
+        from htlab.imagecore import Rng as R, gaussian_noise_map as gmap
+    else:
+        from oracle.htoracle import Rng as R, gaussian_noise_map as gmap
+    n_img = (n + 3) // 4
+    if len(_ref_images) < n_img:
+        rng = R(noise_seed(2))
+        for i in range(n_img):
+            c = synth.contone(S2, S2, seed=noise_seed(2) + i, blobs=8, rects=2,
+                              step_edge=i < round(0.1 * B2))
+            _ref_images[i] = (c, gmap(rng, S2, S2).astype(np.float32))
     jobs = []
-    for k in range(cores):
-        i = k % c.shape[0]
-        y0 = (k * 37) % (c.shape[1] - tile + 1)
-        x0 = (k * 53) % (c.shape[2] - tile + 1)
-        jobs.append((c[i, y0:y0 + tile, x0:x0 + tile].copy(), z[i, y0:y0 + tile, x0:x0 + tile].copy()))
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores, initializer=_cpu_init) as pool:
-        pool.map(_cpu_worker, jobs[:cores])        # warm the workers (imports)
+    for i in range(n_img):
+        c, z = _ref_images[i]
+        for q in range(4):
+            if len(jobs) == n:
+                break
+            y0, x0 = (q // 2) * (S2 - tile), (q % 2) * (S2 - tile)
+            jobs.append((c[y0:y0 + tile, x0:x0 + tile].astype(np.float64),
+                         z[y0:y0 + tile, x0:x0 + tile].astype(np.float64)))
+    return jobs
+
+
+class RefPool:
+    """Worker processes running the reference forward, one BLAS thread each
+    (the limits are exported before the workers are spawned, so OpenBLAS
+    starts single-threaded in every worker)."""
+
+    def __init__(self, cores):
+        import multiprocessing as mp
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"
+        self.kind = "reference" if os.path.isdir(os.path.join(REF_PATH, "htlab")) else "port"
+        init, self.task = ((_ref_worker_init, _ref_task) if self.kind == "reference"
+                           else (_port_worker_init, _port_task))
+        self.cores = cores
+        self.pool = mp.get_context("spawn").Pool(cores, initializer=init, initargs=(REF_PATH,))
+
+    def run(self, jobs):
         t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, jobs)
-        wall = time.perf_counter() - t0
-    px = sum(r[0] for r in res)
-    return px / wall / 1e6, wall, px
+        res = self.pool.map(self.task, jobs, chunksize=1)
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def describe(self, tile, n):
+        what = ("htlab PolicyNetwork.forward + (p >= 0.5) from baseline/_ref (the unmodified "
+                "reference)" if self.kind == "reference" else
+                "oracle/htoracle.py port of nn.py:138-150 + rl.py:311 (reference not installed)")
+        return (f"{n} tiles of {tile}x{tile} px per step (quadrants of config-2 images), one per "
+                f"worker process, {self.cores} processes x 1 BLAS thread: {what}")
 
 
-# ------------------------------------------------------------------ main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=64)
-    ap.add_argument("--size", type=int, default=512)
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-tile", type=int, default=64)
-    ap.add_argument("--workload", default="halftone", choices=["halftone", "train"],
-                    help="halftone = BASELINE config 2 (headline); train = config 5 train_step")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    B, H, W = args.batch, args.size, args.size
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    return rank, world, local
 
-    if args.impl == "reference":
-        return run_reference(args, rank, world, B, H, W)
-    if args.workload == "train":
-        return run_train(args, rank, world, local)
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: one rank per GPU under torch.distributed.run."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class Dist:
+    def __init__(self, rank, world, dev):
+        self.rank, self.world, self.dev = rank, world, dev
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, *vals):
+        import torch
+        t = torch.tensor(vals, dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.cpu()]
+
+
+def timed(D, fn, steps, warmup, stream=None):
+    """Device time of `steps` calls of fn (CUDA events on the launch stream,
+    barrier + synchronize on both sides), max over ranks; returns ms/step."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    D.barrier()
+    st = stream or torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    D.barrier()
+    return D.max(e0.elapsed_time(e1) / steps)[0]
+
+
+# ------------------------------------------------------------------ sub-configs
+def bench_cfg1(D, net, reps):
+    """Config 1: one 256x256 contone, batch 1 -- latency.  Device-resident
+    (inputs in HBM, L2 flushed before each run) and end to end through
+    rl.HalftoneEngine (pinned host in, uint8 out), median of `reps`."""
+    import torch
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_device
+    dev = D.dev
+    c = torch.from_numpy(synth.contone(256, 256, seed=0, blobs=8, rects=2)).to(dev)[None]
+    z = gaussian_noise_map_device(Rng(0), 256, 256, device=dev)[None]
+    h = torch.empty((1, 256, 256), dtype=torch.uint8, device=dev)
+    ws = net.halftone_device(c, z, h_out=h, check=True)
+    st = torch.cuda.current_stream()
+    dev_ms = []
+    with ClockSampler(dev.index) as clk:
+        for _ in range(reps + 3):
+            l2_flush(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            net.halftone_device(c, z, h_out=h, workspace=ws)
+            e1.record(st)
+            torch.cuda.synchronize()
+            dev_ms.append(e0.elapsed_time(e1))
+        eng = rl.HalftoneEngine(net, 1, 256, 256, chunks=1, output="h", depth=1)
+        ch, zh = c.cpu().pin_memory(), z.cpu().pin_memory()
+        oh = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+        e2e_ms = []
+        for _ in range(reps + 3):
+            l2_flush(dev)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng(ch, zh, oh)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    assert torch.equal(oh, h.cpu()), "cfg1: e2e output differs from the device path"
+    return {"workload": "BASELINE config 1: 1 x 256x256 contone (seed 0), batch 1",
+            "latency_ms": round(float(np.median(dev_ms[3:])), 4),
+            "latency_ms_e2e": round(float(np.median(e2e_ms[3:])), 4),
+            "unit": "ms (median, L2 flushed before each run)", "reps": reps,
+            "e2e_api": "rl.HalftoneEngine(B=1) pinned host fp32 in -> uint8 out, wall clock",
+            "clocks": clk.summary()}
+
+
+def bench_cfg3(D, net, steps, warmup):
+    """Config 3: 256 flat-gray 256x256 images g = k/255 with their own noise
+    maps -> forward + binarize, then per-level RAPSD + anisotropy of the
+    halftone (K7) and the anisotropy loss of p (K5).  Levels sharded over the
+    ranks; Mpx/s over all levels (max over ranks)."""
+    import torch
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.parallel import shard_range
+    from paper_2304_12152_b200.spectral import anisotropy_device, rapsd_device, ring_partition
+    dev = D.dev
+    n_lv, S = 256, 256
+    lo, hi = shard_range(n_lv, D.rank, D.world)
+    n = hi - lo
+    g = torch.arange(lo, hi, dtype=torch.float32, device=dev) / 255.0
+    c = g[:, None, None].expand(n, S, S).contiguous()
+    rng = Rng(noise_seed(3))
+    rng.jump(lo * S * S)
+    z = rng.gaussians_device(n * S * S, device=dev).view(n, S, S)
+    part = ring_partition((S, S))
+    p = torch.empty((n, S, S), dtype=torch.float32, device=dev)
+    h = torch.empty((n, S, S), dtype=torch.uint8, device=dev)
+    ws = net.halftone_device(c, z, p_out=p, h_out=h, check=True)
+    hf = torch.empty((n, S, S), dtype=torch.float32, device=dev)
+    out = {}
+
+    def step():
+        net.halftone_device(c, z, p_out=p, h_out=h, workspace=ws)
+        hf.copy_(h)
+        out["spec"] = rapsd_device(hf, part)
+        out["las"] = anisotropy_device(p, part, want_grad=False)[0]
+
+    with ClockSampler(dev.index) as clk:
+        ms = timed(D, step, steps, warmup)
+    power, anis, dc = out["spec"]
+    from paper_2304_12152_b200.spectral import anisotropy_db
+    mean_db = float(np.nanmean(anisotropy_db(anis.cpu().numpy())))
+    return {"workload": "BASELINE config 3: 256 flat-gray 256x256 levels g=k/255, forward + "
+                        "binarize + RAPSD/anisotropy of each halftone + L_AS of each p",
+            "value": round(n_lv * S * S / (ms * 1e-3) / 1e6, 2), "unit": "Mpixel/s",
+            "ms_per_step": round(ms, 4), "steps": steps,
+            "parallelism": f"levels sharded {n_lv}/{D.world} per rank",
+            "mean_anisotropy_db_rank0": round(mean_db, 3),
+            "l2": "inputs (134 MB) larger than L2", "clocks": clk.summary()}
+
+
+def bench_cfg4(D, net, steps, warmup):
+    """Config 4: one 7016x4960 page (64 blobs, 16 rects), row strips over the
+    ranks with a 34-row input halo (no communication; stitched result equals
+    the unsharded one, tests/test_gpu_forward.py).  Device-resident and end
+    to end (the rank's strip of contone+noise from pinned host memory in,
+    its uint8 rows out), max over ranks."""
+    import torch
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.parallel import row_strip
+    dev = D.dev
+    H, W = 7016, 4960
+    st = row_strip(H, D.rank, D.world)
+    page = synth.contone(H, W, seed=4, blobs=64, rects=16)
+    rng = Rng(noise_seed(4))
+    rng.jump(st.in_row0 * W)                         # W even: rows are whole draw pairs
+    z = rng.gaussians_device(st.in_rows * W, device=dev).view(1, st.in_rows, W)
+    c = torch.from_numpy(page[st.in_row0:st.in_row0 + st.in_rows]).to(dev)[None]
+    h = torch.empty((1, st.out_rows, W), dtype=torch.uint8, device=dev)
+    rows = st.as_kernel_rows(H)
+    ws = net.halftone_device(c, z, h_out=h, rows=rows, check=True)
+    ch, zh = c.cpu().pin_memory(), z.cpu().pin_memory()
+    hh = torch.empty(h.shape, dtype=torch.uint8).pin_memory()
+    cd, zd = torch.empty_like(c), torch.empty_like(z)
+
+    def step_dev():
+        net.halftone_device(c, z, h_out=h, rows=rows, workspace=ws)
+
+    def step_e2e():
+        cd.copy_(ch, non_blocking=True)
+        zd.copy_(zh, non_blocking=True)
+        net.halftone_device(cd, zd, h_out=h, rows=rows, workspace=ws)
+        hh.copy_(h, non_blocking=True)
+
+    with ClockSampler(dev.index) as clk:
+        ms = timed(D, step_dev, steps, warmup)
+        ms_e2e = timed(D, step_e2e, steps, warmup)
+    assert torch.equal(hh, h.cpu())
+    return {"workload": "BASELINE config 4: one 7016x4960 page (64 blobs, 16 rects), row strips "
+                        "with 34-row halos",
+            "value": round(H * W / (ms * 1e-3) / 1e6, 2), "unit": "Mpixel/s",
+            "ms_per_page": round(ms, 4),
+            "e2e": {"value": round(H * W / (ms_e2e * 1e-3) / 1e6, 2), "unit": "Mpixel/s",
+                    "h2d_bytes_per_step": 2 * st.in_rows * W * 4, "d2h_bytes_per_step": st.out_rows * W},
+            "steps": steps, "parallelism": f"row strips over {D.world} rank(s), no collective",
+            "l2": "inputs (278 MB) larger than L2", "clocks": clk.summary()}
+
+
+def bench_cfg5(D, steps, warmup, burst):
+    """Config 5: rl.train_step with 16 x 256x256 crops + 4 flat-gray images
+    (LE estimator, Gaussian HVS, anisotropy loss, backward, Adam); data
+    parallel over the ranks with one gradient all-reduce per step."""
+    import torch
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    group = None
+    cfg = rl.TrainConfig(iterations=1000, batch_size=16, crop_size=256, anisotropy_batch_size=4,
+                         hvs_model="gaussian")
+    ds = [synth.contone(384, 384, seed=100 + i).astype(np.float64) for i in range(8)]
+    rng = Rng(cfg.seed)
+    net = PolicyNetwork(cfg.channels, cfg.blocks)
+    adam = Adam(net.params())
+    net.init_params(rng)
+    t = [0]
+    diag = {}
+
+    def step():
+        diag.update(rl.train_step(net, adam, ds, cfg, rng, t[0], group=group))
+        t[0] += 1
+
+    with ClockSampler(D.dev.index) as clk:
+        ms = timed(D, step, steps, warmup)
+    # tensor work of the 32->32 convs: forward, input gradient, weight
+    # gradient, each as six bf16 products of the three-way split operands
+    px = 20 * 256 * 256
+    flop = px * 2 * 9 * 32 * 32 * 32 * 3 * 6
+    return {"workload": "BASELINE config 5: train_step, 16 x 256x256 crops + 4 flat-gray images, "
+                        "LE estimator (Gaussian HVS), anisotropy loss, backward, Adam",
+            "value": round(1e3 / ms, 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
+            "steps": steps, "parallelism": f"data parallel over {D.world} rank(s), one all-reduce per step",
+            "roofline": {"bound": "tensor", "unit": "TFLOP/s",
+                         "achieved": round(flop / (ms * 1e-3) / 1e12, 1), "peak": burst,
+                         "frac": round(flop / (ms * 1e-3) / 1e12 / burst, 4),
+                         "work": "32->32 convs (fwd + dgrad + wgrad) x 6 split-bf16 products, whole step time"},
+            "last_diag": {k: (round(v, 9) if isinstance(v, float) else v) for k, v in diag.items()},
+            "clocks": clk.summary()}
+
+
+# ------------------------------------------------------------------ main arms
+def run_ours(args, rank, world, local):
+    import ctypes as C
 
     import torch
     import torch.distributed as dist
+    from paper_2304_12152_b200.parallel import shard_range
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2304_12152_b200 import _lib, rl
-
     dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    seed = 2 + 7919 * rank
-    c_np, z_np = make_inputs(B, H, W, seed=seed, device=dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2304_12152_b200 import _lib, rl
+    D = Dist(rank, world, dev)
+    burst, sustained, hbm, src = load_peaks()
+
+    lo, hi = shard_range(B2, rank, world)
+    B = hi - lo
+    c_np, z_np = make_inputs(lo, hi, S2, S2, seed=2, device=dev)
     net = make_net()
     c = torch.from_numpy(c_np).to(dev)
     z = torch.from_numpy(z_np).to(dev)
-    h = torch.empty((B, H, W), dtype=torch.uint8, device=dev)
+    h = torch.empty((B, S2, S2), dtype=torch.uint8, device=dev)
     ws = net.halftone_device(c, z, h_out=h, check=True)       # correctness gate + workspace
     torch.cuda.synchronize()
 
@@ -219,64 +538,34 @@ def main():
     for _ in range(args.warmup):
         step()
     launches_per_step = _lib.launch_count()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     _lib.call("ht_timing_reserve", 16 * args.steps)
     _lib.call("ht_timing_enable", 1)
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(args.steps):
-            step()
-        e1.record(st)
-        torch.cuda.synchronize()
+        ms_step = timed(D, step, args.steps, 0)
     _lib.call("ht_timing_enable", 0)
-    if world > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    import ctypes as C
     nmax = 64 * args.steps
-    tags = (C.c_int * nmax)()
-    tms = (C.c_float * nmax)()
-    cnt = C.c_int(0)
+    tags, tms, cnt = (C.c_int * nmax)(), (C.c_float * nmax)(), C.c_int(0)
     _lib.call("ht_timing_read", tags, tms, nmax, C.byref(cnt))
     per_tag = {}
     for i in range(cnt.value):
         per_tag.setdefault(int(tags[i]), []).append(float(tms[i]))
     mid = per_tag.get(MID_TAG, [float("nan")])
-    mid_ms = float(np.mean(mid))
-    t = torch.tensor([ms, mid_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, mid_ms = float(t[0]), float(t[1])
-    ms_step = ms / args.steps
-    px_rank = B * H * W
-    value = px_rank * world / (ms_step * 1e-3) / 1e6
+    mid_ms = D.max(float(np.mean(mid)))[0]
+    value = B2 * S2 * S2 / (ms_step * 1e-3) / 1e6
 
-    # ---- end-to-end through the public API (pinned host in, uint8 out)
+    # ---- end to end through the public API (pinned host in, uint8 out)
     e2e = None
     if not args.no_e2e:
-        # streamed batches, one chunk each: batch i+1's copies run under batch
-        # i's kernels (measured: 1222 Mpx/s streamed vs 1178 for the best
-        # per-call chunking, debug/e2e_sweep.py)
-        eng = rl.HalftoneEngine(net, B, H, W, chunks=1, output="h", depth=2)
+        eng = rl.HalftoneEngine(net, B, S2, S2, chunks=1, output="h", depth=2)
         ch = torch.from_numpy(c_np).pin_memory()
         zh = torch.from_numpy(z_np).pin_memory()
-        oh = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
-        # contones + noise maps from pinned host memory.  (The engine can also
-        # draw the noise on the GPU from an Rng, eng(ch, rng, oh); measured
-        # slower here: the copy engines move the noise for free while device
-        # generation takes SM time from the forward.)
-        # streaming use: batch i+1 is submitted while batch i finishes (its
-        # first copies overlap i's last kernel and read-back); every batch
-        # does its own H2D of contone + noise and D2H of the halftone, and
-        # batch i is waited on before i+2 reuses its output buffer
-        outs = [oh, torch.empty_like(oh).pin_memory()]
+        outs = [torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory() for _ in range(2)]
 
         def stream_batches(n):
+            # batch i+1 is submitted while batch i finishes (its copies overlap
+            # i's kernels); every batch does its own H2D of contone + noise and
+            # D2H of the halftone; batch i is waited on before i+2 reuses its
+            # output buffer
             tickets = []
             for i in range(n):
                 if i >= 2:
@@ -287,153 +576,137 @@ def main():
             return outs[(n - 1) % 2]
 
         stream_batches(args.warmup)
-        if world > 1:
-            dist.barrier()
+        D.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         last = stream_batches(args.steps)
-        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        el = D.max(time.perf_counter() - t0)[0]
         assert np.array_equal(last.numpy(), h.cpu().numpy()), "e2e output differs from device path"
-        e2e = {"value": px_rank * world * args.steps / float(el) / 1e6, "unit": "Mpixel/s",
+        e2e = {"value": round(B2 * S2 * S2 * args.steps / el / 1e6, 3), "unit": "Mpixel/s",
                "h2d_bytes_per_step": eng.h2d_bytes(), "d2h_bytes_per_step": eng.d2h_bytes(),
                "api": "rl.HalftoneEngine.submit/wait (pinned host fp32 contone+noise -> uint8 "
-                      "halftone, batches streamed two deep)"}
+                      "halftone, batches streamed two deep), per rank",
+               "bytes_note": "per rank; summed over ranks the copies are the whole batch"}
 
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+    # ---- weak scaling (secondary): every rank halftones its own 64 images
+    weak = None
+    if world > 1:
+        cw, zw = make_inputs(0, B2, S2, S2, seed=2 + 7919 * rank, device=dev)
+        cw, zw = torch.from_numpy(cw).to(dev), torch.from_numpy(zw).to(dev)
+        hw_ = torch.empty((B2, S2, S2), dtype=torch.uint8, device=dev)
+        wsw = net.halftone_device(cw, zw, h_out=hw_, check=True)
+        msw = timed(D, lambda: net.halftone_device(cw, zw, h_out=hw_, workspace=wsw), args.steps, 2)
+        weak = {"value": round(B2 * world * S2 * S2 / (msw * 1e-3) / 1e6, 2), "unit": "Mpixel/s",
+                "ms_per_step": round(msw, 4), "per_rank_images": B2}
+        del cw, zw, hw_, wsw
 
-    burst, sustained, hbm, src = load_peaks()
-    achieved = FLOP_PER_PX_MIDPASS * px_rank / (mid_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:   # measured DRAM bytes/pixel of this kernel (ncu) x pixels per launch
-            traffic = round(json.load(open(tpath))[str(MID_TAG)]["bytes_per_px"] * px_rank)
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sustained,
-                "unit": "TFLOP/s", "frac": round(achieved / sustained, 4), "traffic": traffic,
-                "kernel": "tc_pass_kernel<false,2,false> (2 residual blocks = 4 convs 32->32)",
-                "traffic_unit": "bytes per launch (DRAM read+write, ncu)",
-                "algorithmic_flop_per_launch": FLOP_PER_PX_MIDPASS * px_rank,
-                "mean_launch_ms": round(mid_ms, 4), "launches_timed": len(mid),
-                "peak_kind": f"sustained bf16/fp16 dense ({src})",
-                "step_frac_of_peak": round(FLOP_PER_PX * px_rank / (ms_step * 1e-3) / 1e12 / sustained, 4),
-                "pass_ms": {str(k): round(float(np.mean(v)), 4) for k, v in sorted(per_tag.items())}}
-
+    # ---- CPU baseline: the real reference on the host cores (rank 0, N=1)
     cpu = None
     if world == 1 and not args.no_cpu:
-        cores = os.cpu_count() or 1
-        v, wall, px = cpu_sample(c_np, z_np, args.cpu_tile, cores)
-        cpu = {"value": round(v, 6), "unit": "Mpixel/s", "cores": cores, "kind": "port",
-               "sample": f"{cores} crops of {args.cpu_tile}x{args.cpu_tile} px of the workload "
-                         f"images, one per worker process (OPENBLAS_NUM_THREADS=1), "
-                         f"oracle/htoracle.py forward+threshold, {wall:.1f} s wall"}
+        cores = host_cores()
+        pool = RefPool(cores)
+        pool.run(ref_tiles(cores, 32))                 # worker start-up / imports
+        jobs = ref_tiles(cores, REF_TILE)
+        px, wall = pool.run(jobs)
+        pool.close()
+        cpu = {"value": round(px / wall / 1e6, 6), "unit": "Mpixel/s", "cores": cores,
+               "kind": pool.kind, "sample": pool.describe(REF_TILE, len(jobs)) + f", {wall:.1f} s wall"}
 
-    out = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16xf16->f32 (fp32 residual)",
-           "data": "synthetic (seeded ramp+blob+rect contones, reference-RNG noise), random-init weights std 0.01",
-           "config": {"workload": f"BASELINE config 2: {B} x {H}x{W} contones per GPU, policy CNN C=32 B=16",
-                      "global_batch": B * world, "image": [H, W], "parallelism": f"images sharded, {world} rank(s), no collective",
-                      "l2": "inputs (134 MB) + pass buffers (4.3 GB) larger than L2 (126 MB)"},
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": launches_per_step * args.steps,
-           "clocks": clk.summary()}
-    print(json.dumps(out))
-    if world > 1:
-        dist.destroy_process_group()
+    # ---- other BASELINE configs
+    configs = {}
+    if not args.no_configs:
+        sub_steps = max(3, min(args.steps, 10))
+        configs["cfg1"] = bench_cfg1(D, net, reps=20)
+        configs["cfg3"] = bench_cfg3(D, net, sub_steps, 2)
+        configs["cfg4"] = bench_cfg4(D, net, sub_steps, 2)
+        configs["cfg5"] = bench_cfg5(D, sub_steps, 3, burst)
 
-
-def run_train(args, rank, world, local):
-    """BASELINE config 5: one rl.train_step = batch 16 of 256x256 crops + 4
-    flat-gray images, forward, LE estimator (Gaussian HVS), anisotropy loss,
-    backward, Adam; data parallel over the ranks with one all-reduce."""
-    import torch
-    import torch.distributed as dist
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2304_12152_b200 import rl, synth
-    from paper_2304_12152_b200.imagecore import Rng
-    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
-    cfg = rl.TrainConfig(iterations=1000, batch_size=16, crop_size=256, anisotropy_batch_size=4,
-                         hvs_model="gaussian")
-    ds = [synth.contone(384, 384, seed=100 + i).astype(np.float64) for i in range(8)]
-    rng = Rng(cfg.seed)
-    net = PolicyNetwork(cfg.channels, cfg.blocks)
-    adam = Adam(net.params())
-    net.init_params(rng)
-    for t in range(args.warmup):
-        rl.train_step(net, adam, ds, cfg, rng, t)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    # CUDA events on the step stream (they include any host gaps of the step)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for t in range(args.steps):
-        diag = rl.train_step(net, adam, ds, cfg, rng, args.warmup + t)
-    e1.record()
-    torch.cuda.synchronize()
-    el = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
     if rank == 0:
-        ms = float(el) / args.steps
-        print(json.dumps({"metric": "train steps/s (config 5: 16x256^2 + 4 gray, LE + anisotropy, Adam)",
-                          "value": round(1e3 / ms, 3), "unit": "steps/s", "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
-                          "higher_is_better": True, "scaling": "strong",
-                          "dtype": "f32 (32->32 convs: tcgen05 split-bf16, fp32-level; others fp32/fp64)",
-                          "last_diag": diag}))
+        achieved = FLOP_PER_PX_MIDPASS * B * S2 * S2 / (mid_ms * 1e-3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:   # measured DRAM bytes/pixel of this kernel (ncu) x pixels per launch
+                traffic = round(json.load(open(tpath))[str(MID_TAG)]["bytes_per_px"] * B * S2 * S2)
+            except Exception:
+                traffic = None
+        roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": burst,
+                    "unit": "TFLOP/s", "frac": round(achieved / burst, 4), "traffic": traffic,
+                    "kernel": "tc_pass_kernel<false,2,false> (2 residual blocks = 4 convs 32->32)",
+                    "traffic_unit": "bytes per launch (DRAM read+write, ncu)",
+                    "algorithmic_flop_per_launch": FLOP_PER_PX_MIDPASS * B * S2 * S2,
+                    "mean_launch_ms": round(mid_ms, 4), "launches_timed": len(mid),
+                    "peak_kind": f"burst bf16/fp16 dense ({src}); sustained {sustained}",
+                    "frac_of_sustained": round(achieved / sustained, 4),
+                    "step_frac_of_peak": round(FLOP_PER_PX * B2 * S2 * S2 / world / (ms_step * 1e-3) / 1e12 / burst, 4),
+                    "pass_ms": {str(k): round(float(np.mean(v)), 4) for k, v in sorted(per_tag.items())}}
+        out = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f16xf16->f32 (fp32 residual)",
+               "data": "synthetic (seeded ramp+blob+rect contones, reference-RNG noise), random-init weights std 0.01",
+               "config": headline_config(world),
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": launches_per_step * args.steps,
+               "clocks": clk.summary()}
+        if weak is not None:
+            out["weak_scaling"] = weak
+        if configs:
+            out["configs"] = configs
+        print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_reference(args, rank, world, B, H, W):
-    """Reference arm: the reference's CPU path (oracle port of htlab's forward +
-    threshold; the reference is pure Python/NumPy) on the host's cores."""
+def run_reference(args, rank, world):
+    """Reference arm: the unmodified reference (htlab from baseline/_ref)
+    forward + threshold on the host cores; rank 0 only."""
     if rank != 0:
         return
-    c_np, z_np = make_inputs(min(B, 8), H, W, seed=2)
-    cores = os.cpu_count() or 1
-    import multiprocessing as mp
-    tile = args.cpu_tile
-    jobs = []
-    for k in range(cores):
-        i = k % c_np.shape[0]
-        y0 = (k * 37) % (H - tile + 1)
-        x0 = (k * 53) % (W - tile + 1)
-        jobs.append((c_np[i, y0:y0 + tile, x0:x0 + tile].copy(), z_np[i, y0:y0 + tile, x0:x0 + tile].copy()))
-    ctx = mp.get_context("spawn")
-    times = []
-    with ctx.Pool(cores, initializer=_cpu_init) as pool:
-        for s in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            pool.map(_cpu_worker, jobs)
-            if s >= args.warmup:
-                times.append(time.perf_counter() - t0)
-    px = cores * tile * tile
+    cores = host_cores()
+    pool = RefPool(cores)
+    warm = ref_tiles(cores, 32)
+    jobs = ref_tiles(cores, REF_TILE)
+    for _ in range(args.warmup):                 # worker start-up, imports, BLAS init
+        pool.run(warm)
+    times, px = [], 0
+    for _ in range(args.steps):
+        px, wall = pool.run(jobs)
+        times.append(wall)
+    pool.close()
     ms = float(np.mean(times)) * 1e3
     value = px / (ms * 1e-3) / 1e6
+    sample = pool.describe(REF_TILE, len(jobs)) + "; warm-up steps use 32x32 tiles"
     out = {"metric": METRIC, "value": round(value, 6), "unit": "Mpixel/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (same generator/weights as the GPU arm)",
-           "config": {"workload": f"BASELINE config 2 images, bounded sample per step: {cores} x {tile}x{tile} px crops",
-                      "global_batch": B, "image": [H, W]},
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (same generator, noise stream and weights as the GPU arm)",
+           "config": headline_config(world),
            "impl": "reference",
-           "cpu_baseline": {"value": round(value, 6), "unit": "Mpixel/s", "cores": cores, "kind": "port",
-                            "sample": f"{cores} worker processes x one {tile}x{tile} crop per step "
-                                      "(oracle/htoracle.py: NumPy restatement of nn.py:138-150 + rl.py:311)"},
+           "cpu_baseline": {"value": round(value, 6), "unit": "Mpixel/s", "cores": cores,
+                            "kind": pool.kind, "sample": sample},
            "e2e": {"value": round(value, 6), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="headline config 2 only")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

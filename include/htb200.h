@@ -228,6 +228,29 @@ int ht_reinforce_signal(const float *p_dev, const float *m_dev, int B, int64_t n
                         const double *reward_dev, double baseline, double scale,
                         float *signal_out_dev, void *stream);
 
+/* Drop-in RewardContext (metrics.py:165-204, region "full") on float64
+ * action maps h and contones c, computed in float64: maps_out (B,8,H,W) =
+ * e, mu_h, shc, mu_c, scc, sigma_c, ssim, shh; extra_out (B,7,H,W) = f_h,
+ * f_c, luminance, contrast, structure, cssim_map, reward_map (may be NULL);
+ * sums_out (B,2) = sum e^2, sum cssim; h_out (B,H,W) scratch copy of h.  */
+int ht_reward_context_f64(const double *h_dev, const double *c_dev, int B,
+                          int H, int W, const double *k_hvs_dev, int ks,
+                          const double *w_ssim_dev, int wsz, double w_s,
+                          double c1, double c2, double gain,
+                          double *maps_out_dev, double *extra_out_dev,
+                          double *sums_out_dev, double *h_out_dev,
+                          void *stream);
+/* Drop-in delta_map (metrics.py:333-392) in float64: delta_out (B,H,W) =
+ * R(h with pixel a -> other[a]) - R(h).  Workspace:
+ * ht_reward_workspace_bytes(B,H,W) + 8*B*H*W bytes.                      */
+int ht_reward_delta_f64(const double *h_dev, const double *other_dev,
+                        const double *c_dev, int B, int H, int W,
+                        const double *k_hvs_dev, int ks,
+                        const double *w_ssim_dev, int wsz, double w_s,
+                        double c1, double c2, double gain,
+                        double *delta_out_dev, void *workspace_dev,
+                        int64_t workspace_bytes, void *stream);
+
 /* ---- K5 / K7: spectral ---------------------------------------------------
  * anisotropy_loss / anisotropy_loss_backward (spectral.py:100-133) for B
  * images: loss_out (B) float64, grad_out (B,H,W) float32 = dL/dx * scale.
@@ -240,12 +263,48 @@ int ht_anisotropy(const float *x_dev, int B, int H, int W,
                   int n_rings, double scale, double *loss_out_dev,
                   float *grad_out_dev, void *workspace_dev,
                   int64_t workspace_bytes, void *stream);
+/* Same for float64 images (spectral.anisotropy_loss on float64 arrays
+ * keeps the reference's precision); grad_out (B,H,W) float64.           */
+int ht_anisotropy_f64(const double *x_dev, int B, int H, int W,
+                      const int32_t *ring_dev, const int32_t *counts_dev,
+                      int n_rings, double scale, double *loss_out_dev,
+                      double *grad_out_dev, void *workspace_dev,
+                      int64_t workspace_bytes, void *stream);
 /* rapsd (spectral.py:74-88) of the periodogram (spectral.py:17-24) of B
  * images: power_out / anis_out (B, n_rings) float64, dc_out (B).        */
 int ht_rapsd(const float *x_dev, int B, int H, int W,
              const int32_t *ring_dev, const int32_t *counts_dev, int n_rings,
              double *power_out_dev, double *anis_out_dev, double *dc_out_dev,
              void *workspace_dev, int64_t workspace_bytes, void *stream);
+int ht_rapsd_f64(const double *x_dev, int B, int H, int W,
+                 const int32_t *ring_dev, const int32_t *counts_dev, int n_rings,
+                 double *power_out_dev, double *anis_out_dev, double *dc_out_dev,
+                 void *workspace_dev, int64_t workspace_bytes, void *stream);
+/* periodogram (spectral.py:17-24): P_out (B,H,W) float64 = |FFT2(x)|^2/N.
+ * Workspace: ht_spectral_workspace_bytes(B, H, W, 1).                   */
+int ht_periodogram_f64(const double *x_dev, int B, int H, int W,
+                       double *P_out_dev, void *workspace_dev,
+                       int64_t workspace_bytes, void *stream);
+/* rapsd(p_hat, part) (spectral.py:74-88) of given periodograms P (B,H,W). */
+int ht_rapsd_power_f64(const double *P_dev, int B, int H, int W,
+                       const int32_t *ring_dev, const int32_t *counts_dev,
+                       int n_rings, double *power_out_dev,
+                       double *anis_out_dev, double *dc_out_dev,
+                       void *workspace_dev, int64_t workspace_bytes,
+                       void *stream);
+
+/* ---- drop-in layer API in float64 (nn.py:36-103) ------------------------
+ * Conv2d.forward: out (B,Co,H,W) = bias + x (B,Ci,H,W) correlated with w
+ * (Co,Ci,3,3), zero padding 1 (nn.py:46-60).  bias may be NULL.
+ * Conv2d.backward (nn.py:62-77): dw (Co,Ci,3,3) += dL/dw, db (Co) += dL/db
+ * (both may be NULL), dx (B,Ci,H,W) = dL/dx (may be NULL).              */
+int ht_conv3x3_f64(const double *x_dev, int B, int Ci, int Co, int H, int W,
+                   const double *w_dev, const double *bias_dev,
+                   double *out_dev, void *stream);
+int ht_conv3x3_f64_backward(const double *x_dev, const double *dout_dev,
+                            int B, int Ci, int Co, int H, int W,
+                            const double *w_dev, double *dw_dev,
+                            double *db_dev, double *dx_dev, void *stream);
 
 /* ---- K6: Adam (nn.py:163-186) on the flat float64 parameter vector ----- */
 int ht_adam_step(double *params_dev, const double *grad_dev, double *m_dev,

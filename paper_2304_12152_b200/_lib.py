@@ -62,6 +62,16 @@ SIGNATURES = {
     "ht_spectral_workspace_bytes": [_i, _i, _i, _i, _i64p],
     "ht_anisotropy": [_vp, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp, _i64, _vp],
     "ht_rapsd": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _vp],
+    "ht_anisotropy_f64": [_vp, _i, _i, _i, _vp, _vp, _i, _d, _vp, _vp, _vp, _i64, _vp],
+    "ht_rapsd_f64": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _vp],
+    "ht_periodogram_f64": [_vp, _i, _i, _i, _vp, _vp, _i64, _vp],
+    "ht_rapsd_power_f64": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _vp],
+    "ht_reward_context_f64": [_vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _d, _d, _d, _d, _vp, _vp,
+                              _vp, _vp, _vp],
+    "ht_reward_delta_f64": [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _d, _d, _d, _d, _vp, _vp,
+                            _i64, _vp],
+    "ht_conv3x3_f64": [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
+    "ht_conv3x3_f64_backward": [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "ht_adam_step": [_vp, _vp, _vp, _vp, _i64, _i, _d, _d, _d, _d, _vp],
     "ht_bin_gap_sum": [_vp, _i64, _vp, _vp],
 }

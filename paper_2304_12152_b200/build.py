@@ -54,7 +54,10 @@ def build(force=False, verbose=False):
         raise RuntimeError("CUDA build failed")
     if procs or force or not os.path.exists(OUT) or any(
             os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
+        # cuFFT (K5/K7's 2-D transforms) from the CUDA toolkit, found at run
+        # time through the rpath (the GPU boxes run the same image)
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", *objs,
+               "-L/usr/local/cuda/lib64", "-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
                "-o", OUT]
         subprocess.run(cmd, check=True)
     return OUT

@@ -4,11 +4,63 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
 
 namespace ht {
+
+int ensure_smem_attr(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, uint64_t> done;   // kernel -> device bit mask
+  int dev = 0;
+  HT_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lk(mu);
+  uint64_t &mask = done[kernel];
+  if (!(mask & bit)) {
+    HT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    mask |= bit;
+  }
+  return HT_OK;
+}
+
+namespace {
+struct BiasEntry {
+  uint64_t gen = 0, seen = ~0ull;
+  cudaEvent_t packed = nullptr;     // recorded on the packing stream
+  std::vector<float> host;
+};
+std::mutex g_bias_mu;
+std::unordered_map<const void *, BiasEntry> g_bias;
+}  // namespace
+
+int note_bias_pack(const void *tcb_dev, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_bias_mu);
+  BiasEntry &e = g_bias[tcb_dev];
+  e.gen++;
+  if (!e.packed) HT_CUDA(cudaEventCreateWithFlags(&e.packed, cudaEventDisableTiming));
+  HT_CUDA(cudaEventRecord(e.packed, st));
+  return HT_OK;
+}
+
+int host_biases(const float *tcb_dev, int64_t n, cudaStream_t st, const float **out) {
+  (void)st;
+  std::lock_guard<std::mutex> lk(g_bias_mu);
+  BiasEntry &e = g_bias[tcb_dev];
+  if (e.seen != e.gen || (int64_t)e.host.size() != n) {
+    // after the pack that wrote them, whatever stream it ran on
+    e.host.resize(n);
+    if (e.packed) HT_CUDA(cudaEventSynchronize(e.packed));
+    HT_CUDA(cudaMemcpy(e.host.data(), tcb_dev, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    e.seen = e.gen;
+  }
+  *out = e.host.data();
+  return HT_OK;
+}
 
 static thread_local char g_err[1024] = "";
 static thread_local int g_launches = 0;

@@ -47,6 +47,20 @@ bool timing_enabled();
 void timing_mark_begin(cudaStream_t st, int tag);
 void timing_mark_end(cudaStream_t st);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the device context, so a process driving several
+// GPUs must set it on each of them.
+int ensure_smem_attr(const void *kernel, int bytes);
+
+// Host copy of a packed network's fp32 bias section (ht_pack_params writes it
+// on the device).  The fused forward passes each pass's biases as kernel
+// parameters, so concurrent forwards of different networks on different
+// streams never share a mutable constant bank.  The copy is refreshed (wait
+// for the event ht_pack_params recorded after its pack, then a 4 KB D2H) only
+// after ht_pack_params rewrote the section.
+int note_bias_pack(const void *tcb_dev, cudaStream_t st);
+int host_biases(const float *tcb_dev, int64_t n, cudaStream_t st, const float **out);
+
 // Offsets of the parameter tensors in the flat params() vector
 // (nn.py:118-122): conv_in, then per block conv1 / conv2, then conv_out.
 struct NetGeom {

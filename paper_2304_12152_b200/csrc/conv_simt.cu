@@ -352,12 +352,7 @@ static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, do
     // the tensor-core kernel streams rows with TMA (16-B row strides: W % 4 == 0)
     if (g_train_conv_impl == 0 && W % 4 == 0) return wgrad_tc32(x, dout, B, H, W, dw, db, g_wgrad_parts, st);
     const size_t smem = sizeof(float) * ((size_t)32 * (W32_TY + 2) * (W32_TX + 2) + W32_TY * W32_TX * W32_PAD);
-    static bool attr32 = false;
-    if (!attr32) {
-      HT_CUDA(cudaFuncSetAttribute(conv3x3_wgrad32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr32 = true;
-    }
+    if (int rc = ensure_smem_attr((const void *)conv3x3_wgrad32_kernel, (int)smem)) return rc;
     const long tiles = (long)B * ((W + W32_TX - 1) / W32_TX) * ((H + W32_TY - 1) / W32_TY);
     const int per = tiles > 148 * 2 ? (int)((tiles + 148 * 2 - 1) / (148 * 2)) : 1;
     const int grid = (int)((tiles + per - 1) / per);
@@ -368,12 +363,7 @@ static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, do
   }
   constexpr int NT = WgSimt<CIN, COUT>::NT;
   const size_t smem = sizeof(float) * ((size_t)CIN * (WT_Y + 2) * (WT_X + 2) + WT_Y * WT_X * WgSimt<CIN, COUT>::DP);
-  static bool attr_set = false;
-  if (!attr_set) {
-    HT_CUDA(cudaFuncSetAttribute(conv3x3_wgrad_kernel<CIN, COUT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  if (int rc = ensure_smem_attr((const void *)conv3x3_wgrad_kernel<CIN, COUT>, (int)smem)) return rc;
   const long tiles = (long)B * ((W + WT_X - 1) / WT_X) * ((H + WT_Y - 1) / WT_Y);
   const int per = tiles > 148 * 8 ? (int)((tiles + 148 * 8 - 1) / (148 * 8)) : 1;
   const int grid = (int)((tiles + per - 1) / per);

@@ -506,12 +506,8 @@ extern "C" int ht_debug_conv_timeline(long long *host) {
 int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
               const float *resid, float *out, int relu, cudaStream_t st) {
   using namespace tct;
-  static bool attr = false;
-  if (!attr) {
-    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LDG));
-    HT_CUDA(cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TMA));
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr((const void *)conv_tc_kernel<false>, SMEM_LDG)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc_kernel<true>, SMEM_TMA)) return rc;
   int dev = 0, n_sm = 148;
   HT_CUDA(cudaGetDevice(&dev));
   HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));

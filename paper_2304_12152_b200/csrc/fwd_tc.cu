@@ -204,7 +204,7 @@ static_assert(PLANE == 2176, "mma_row's A chunk offset assumes PLANE == 2176");
 // ---------------------------------------------------------------------------
 struct TcParams {
   const uint8_t *w;     // this pass's weight tiles (same byte image as smem)
-  int layer0;           // index of the pass's first layer in c_bias
+  int layer0;           // index of the pass's first layer (0 = conv_in)
   const float *c, *z;   // HI: (B, rows, W) fp32 planes
   const float *x_in;    // !HI: (rows, 8, VW, 4) fp32 (channel-group planar)
   float *x_out;         // !HO: (rows, 8, VW, 4) fp32
@@ -219,14 +219,14 @@ struct TcParams {
                         // the strip-major (strip, row) space, split into segments
   int out_rows;         // HO: rows of p/h (== r_hi - r_lo)
   int steps;            // HO: output lattice i/steps (1 = binary halftone)
+  // this pass's biases (<= 4 layers x 32), read from the kernel-parameter
+  // constant bank (not SMEM: the tensor core's operand reads saturate
+  // shared-memory bandwidth).  Per launch, so concurrent forwards of
+  // different networks never share mutable state.
+  float bias[4][32];
 };
 
-// Biases live in the constant bank (not SMEM: the tensor core's operand reads
-// saturate shared-memory bandwidth and starve LSU loads).  Filled per
-// ht_halftone call with a stream-ordered device->constant copy.
-constexpr int MAX_BIAS = 64 * 32;
-__constant__ float c_bias[MAX_BIAS];
-#define PBIAS(j, i) c_bias[(P.layer0 + (j)) * 32 + (i)]
+#define PBIAS(j, i) P.bias[(j)][(i)]
 
 // One 4-warp group per layer (128 threads = the 128 pixel lanes of a strip
 // row; warp k of a group owns TMEM lane quarter k; each thread owns one pixel
@@ -695,11 +695,7 @@ static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
   static_assert(PL::TCOLS <= 512, "TMEM columns exceeded");
   static_assert(PL::SMEM <= 232448, "shared memory exceeded");
   auto kern = tc_pass_kernel<HI, NBK, HO>;
-  static bool attr = false;
-  if (!attr) {
-    HT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM));
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr((const void *)kern, PL::SMEM)) return rc;
   timing_mark_begin(st, (HI ? 100 : 0) + NBK * 10 + (HO ? 1 : 0));
   kern<<<grid, 128 * PL::G, PL::SMEM, st>>>(prm);
   timing_mark_end(st);
@@ -722,7 +718,11 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
   float *xa = (float *)ws;
   float *xb = xa + (size_t)in_rows * x_pitch(VW) * 32;
   // pass plan (layers: conv_in, 2*NB convs, conv_out)
-  PassDesc passes[64];
+  constexpr int MAX_PASSES = 64;
+  HT_REQUIRE(NB / 2 + 2 <= MAX_PASSES, "too many residual blocks for the fused forward (%d)", NB);
+  const float *hb = nullptr;
+  if (int rc = host_biases(tc_b, bias_floats(NB), st, &hb)) return rc;
+  PassDesc passes[MAX_PASSES];
   int np = 0;
   {
     // <= 4 layers per pass: conv_in + 1 block | 2 blocks ... | <=1 block + conv_out
@@ -732,9 +732,6 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     while (NB - done > 1) { passes[np++] = {false, false, 2, 1 + 2 * done}; done += 2; }
     passes[np++] = {false, true, NB - done, 1 + 2 * done};
   }
-  HT_REQUIRE(bias_floats(NB) <= MAX_BIAS, "too many layers for the bias bank");
-  HT_CUDA(cudaMemcpyToSymbolAsync(c_bias, tc_b, sizeof(float) * bias_floats(NB), 0,
-                                  cudaMemcpyDeviceToDevice, st));
   const uint8_t *wbase = (const uint8_t *)tc_w;
   const float *in_x = nullptr;
   float *out_x = xa;
@@ -744,6 +741,8 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     TcParams prm{};
     prm.w = wbase + (pd.layer0 == 0 ? 0 : weight_offset_mid(pd.layer0 - 1));
     prm.layer0 = pd.layer0;
+    for (int j = 0; j < G; ++j)
+      for (int i = 0; i < 32; ++i) prm.bias[j][i] = hb[(pd.layer0 + j) * 32 + i];
     prm.c = c; prm.z = z;
     prm.x_in = in_x;
     prm.x_out = pd.ho ? nullptr : out_x;

@@ -77,6 +77,8 @@ int ht_pack_params(const double *params, int C, int NB, void *packed, void *stre
   if (C == ht::tc::C) {
     int rc = ht::tc::pack(params, NB, base + L.tc_off, (float *)(base + L.tcb_off), st);
     if (rc) return rc;
+    rc = ht::note_bias_pack(base + L.tcb_off, st);
+    if (rc) return rc;
   }
   return HT_OK;
 }

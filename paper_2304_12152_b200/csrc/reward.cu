@@ -27,7 +27,7 @@ constexpr int RMAXK = 11;         // max stencil size supported (odd; the refere
 constexpr int RH = RMAXK / 2;     // max halo
 
 __device__ __forceinline__ double ssim3(double mx, double my, double sxx, double syy, double sxy,
-                                        double c1, double c2) {
+                                        double c1, double c2, double *parts = nullptr) {
   // metrics.py:95-107
   const double vx = fmax(sxx - mx * mx, 0.0);
   const double vy = fmax(syy - my * my, 0.0);
@@ -37,10 +37,19 @@ __device__ __forceinline__ double ssim3(double mx, double my, double sxx, double
   const double lum = (2.0 * mx * my + c1) / (mx * mx + my * my + c1);
   const double con = (2.0 * sx * sy + c2) / (vx + vy + c2);
   const double str = (cov + c3) / (sx * sy + c3);
+  if (parts) {
+    parts[0] = lum;
+    parts[1] = con;
+    parts[2] = str;
+  }
   return lum * con * str;
 }
 
 constexpr int NMAPS = 8;
+// RewardContext's remaining maps (metrics.py:188-204), written on request:
+//   [0] f_h  [1] f_c  [2] luminance  [3] contrast  [4] structure
+//   [5] cssim_map  [6] reward_map
+constexpr int NEXTRA = 7;
 
 // two-point cast (rl.py:40-57): floor / ceil lattice values and upper mass
 __device__ __forceinline__ void cast_two_point(double v, int steps, double &fl, double &ce, double &frac) {
@@ -53,13 +62,16 @@ __device__ __forceinline__ void cast_two_point(double v, int steps, double &fl, 
 
 // Stage 1: per pixel maps.  Workspace layout per image (doubles, n = H*W):
 //   [0] e  [1] mu_h  [2] shc  [3] mu_c  [4] scc  [5] sigma_c  [6] ssim  [7] shh
-// plus per-image sums[2] = {sum e^2, sum cssim}.  Also writes m.
+// plus per-image sums[2] = {sum e^2, sum cssim}.  Also writes m, and the
+// NEXTRA maps of the drop-in RewardContext when `extra` is given.  T is the
+// input type: float32 on the training path, float64 for the drop-in API.
+template <typename T>
 __global__ void __launch_bounds__(256)
-reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
-                   const float *__restrict__ c, int H, int W, const double *__restrict__ k,
+reward_maps_kernel(const T *__restrict__ p, const double *__restrict__ u,
+                   const T *__restrict__ c, int H, int W, const double *__restrict__ k,
                    int ks, const double *__restrict__ w, int wsz, double c1, double c2,
-                   double gain, double w_s, int steps, float *__restrict__ m_out,
-                   double *__restrict__ maps, double *__restrict__ sums) {
+                   double gain, double w_s, int steps, T *__restrict__ m_out,
+                   double *__restrict__ maps, double *__restrict__ sums, double *__restrict__ extra) {
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
   const int hk = ks / 2, hw = wsz / 2, hh = hk > hw ? hk : hw;
@@ -69,9 +81,9 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
   __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
   __shared__ double red[2][8];
   const size_t n = (size_t)H * W;
-  const float *pb = p + b * n;
+  const T *pb = p + b * n;
   const double *ub = u + b * n;
-  const float *cb = c + b * n;
+  const T *cb = c + b * n;
   for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
   for (int i = threadIdx.x; i < wsz * wsz; i += 256) sw[i] = w[i];
   for (int i = threadIdx.x; i < TP * TP; i += 256) {
@@ -120,7 +132,8 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
         scc += wv * (cv * cv);
       }
     const double sig = fmin(gain * sqrt(fmax(scc - muc * muc, 0.0)), 1.0);
-    const double s = ssim3(muh, muc, shh, scc, shc, c1, c2);
+    double parts[3];
+    const double s = ssim3(muh, muc, shh, scc, shc, c1, c2, parts);
     const double e = fh - fc;
     const size_t idx = (size_t)gy * W + gx;
     double *mb = maps + (size_t)b * NMAPS * n;
@@ -132,9 +145,19 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
     mb[5 * n + idx] = sig;
     mb[6 * n + idx] = s;
     mb[7 * n + idx] = shh;
-    m_out[b * n + idx] = (float)sm[ty + RH][tx + RH];
+    m_out[b * n + idx] = (T)sm[ty + RH][tx + RH];
     e2 = e * e;
     cs = sig * s + (1.0 - sig);
+    if (extra) {
+      double *xb = extra + (size_t)b * NEXTRA * n;
+      xb[0 * n + idx] = fh;
+      xb[1 * n + idx] = fc;
+      xb[2 * n + idx] = parts[0];
+      xb[3 * n + idx] = parts[1];
+      xb[4 * n + idx] = parts[2];
+      xb[5 * n + idx] = cs;
+      xb[6 * n + idx] = -e2 + w_s * cs;
+    }
   }
   (void)hh;
   for (int o = 16; o > 0; o >>= 1) {
@@ -157,11 +180,12 @@ reward_maps_kernel(const float *__restrict__ p, const double *__restrict__ u,
 // Stage 2: delta for moving every pixel to its other support point, then
 // the estimator's signal (scaled), per pixel a.  estimator: 0 = local
 // expectation, 1 = COMA (binary only).
+template <typename T, typename TO>
 __global__ void __launch_bounds__(256)
-reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ p, const float *__restrict__ other,
-                 const float *__restrict__ c, int H, int W, const double *__restrict__ k, int ks, const double *__restrict__ w, int wsz,
+reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *__restrict__ other,
+                 const T *__restrict__ c, int H, int W, const double *__restrict__ k, int ks, const double *__restrict__ w, int wsz,
                  double c1, double c2, double w_s, double scale, int steps, int estimator,
-                 const double *__restrict__ maps, float *__restrict__ signal) {
+                 const double *__restrict__ maps, TO *__restrict__ signal) {
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
   const int hk = ks / 2, hw = wsz / 2;
@@ -186,15 +210,15 @@ reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ p, co
   const int gy = y0 + ty, gx = x0 + tx;
   if (gy >= H || gx >= W) return;
   const size_t ia = (size_t)gy * W + gx;
-  const float mf = m_in[b * n + ia];
+  const T mf = m_in[b * n + ia];
   double ma = (double)mf;
   const double ca = (double)c[b * n + ia];
   // other support point (rl.py:98-99): m == ceil ? floor : ceil
   const double pa = (double)p[b * n + ia];
   double lv, hv, frac;
   cast_two_point(pa, steps, lv, hv, frac);
-  // m_out is float32: recover the exact lattice value of a sampled action
-  const bool at_ceil = mf == (float)hv;
+  // m_out may be float32: recover the exact lattice value of a sampled action
+  const bool at_ceil = mf == (T)hv;
   if (!other) ma = at_ceil ? hv : lv;
   // other - h: the given substitution, or the other support point (+-1 for
   // L=2; 0 where the support collapsed)
@@ -216,7 +240,10 @@ reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ p, co
   // dCS[a] = sum over window centres b = a - (dy,dx), in image, of
   //          sigma_c[b] (SSIM_b(after) - SSIM_b(before)),  wd = w[hw+dy, hw+dx]
   double dcs = 0.0;
-  if (w_s != 0.0) {
+  // d == 0: the window statistics do not move, so every SSIM term cancels
+  // exactly (as in the reference's numpy evaluation; recomputing s1 here
+  // could differ from the stored s0 in the last bit)
+  if (w_s != 0.0 && d != 0.0) {
     const double dh = 2.0 * ma * d + d * d;
     for (int dy = -hw; dy <= hw; ++dy) {
       const int by = gy - dy;
@@ -246,7 +273,7 @@ reward_le_kernel(const float *__restrict__ m_in, const float *__restrict__ p, co
     // local expectation: -(sign * delta) / (1/(L-1)), sign = -1 where m == ceil
     sigv = (at_ceil ? delta : -delta) * (double)steps;
   }
-  signal[b * n + ia] = (float)(sigv * scale);
+  signal[b * n + ia] = (TO)(sigv * scale);
 }
 
 __global__ void reinforce_kernel(const float *__restrict__ p, const float *__restrict__ m, int64_t total,
@@ -299,13 +326,13 @@ int ht_reward_signal(const float *p, const double *u, const float *other, const 
   double *sums = maps + (size_t)B * ht::NMAPS * H * W;
   HT_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 2 * B, st));
   dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
-  ht::reward_maps_kernel<<<grid, 256, 0, st>>>(p, u, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s, levels - 1,
-                                               m_out, maps, sums);
+  ht::reward_maps_kernel<float><<<grid, 256, 0, st>>>(p, u, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s,
+                                                      levels - 1, m_out, maps, sums, nullptr);
   ht::count_launch();
   HT_CHECK_LAUNCH();
   if (signal_out) {
-    ht::reward_le_kernel<<<grid, 256, 0, st>>>(m_out, p, other, c, H, W, k, ks, w, wsz, c1, c2, w_s, scale, levels - 1,
-                                                estimator, maps, signal_out);
+    ht::reward_le_kernel<float, float><<<grid, 256, 0, st>>>(m_out, p, other, c, H, W, k, ks, w, wsz, c1, c2,
+                                                             w_s, scale, levels - 1, estimator, maps, signal_out);
     ht::count_launch();
     HT_CHECK_LAUNCH();
   }
@@ -324,6 +351,56 @@ int ht_reward_le(const float *p, const double *u, const float *c, int B, int H, 
                  double *reward_out, void *ws, int64_t ws_bytes, void *stream) {
   return ht_reward_signal(p, u, nullptr, c, B, H, W, k, ks, w, wsz, w_s, c1, c2, gain, 2, 0, scale, m_out,
                           signal_out, reward_out, ws, ws_bytes, stream);
+}
+
+// Drop-in RewardContext (metrics.py:165-204) on float64 action maps h and
+// contones c (region "full"): maps_out (B, 8, H, W) = e, mu_h, shc, mu_c,
+// scc, sigma_c, ssim, shh; extra_out (B, 7, H, W) = f_h, f_c, luminance,
+// contrast, structure, cssim_map, reward_map; sums_out (B, 2) = sum e^2,
+// sum cssim; h_out (B, H, W) a copy of the action maps (scratch).
+int ht_reward_context_f64(const double *h, const double *c, int B, int H, int W, const double *k, int ks,
+                          const double *w, int wsz, double w_s, double c1, double c2, double gain,
+                          double *maps_out, double *extra_out, double *sums_out, double *h_out,
+                          void *stream) {
+  HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty batch");
+  HT_REQUIRE(ks % 2 == 1 && ks <= ht::RMAXK && wsz % 2 == 1 && wsz <= ht::RMAXK,
+             "stencils must be odd and at most %d wide", ht::RMAXK);
+  HT_REQUIRE(maps_out && sums_out && h_out, "maps_out, sums_out and h_out are required");
+  cudaStream_t st = (cudaStream_t)stream;
+  HT_CUDA(cudaMemsetAsync(sums_out, 0, sizeof(double) * 2 * B, st));
+  dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
+  ht::reward_maps_kernel<double><<<grid, 256, 0, st>>>(h, nullptr, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s, 1,
+                                                       h_out, maps_out, sums_out, extra_out);
+  ht::count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+// Drop-in delta_map (metrics.py:333-392) in float64: delta_out[a] =
+// R(h with pixel a -> other[a]) - R(h) for every pixel a.  Workspace:
+// ht_reward_workspace_bytes(B, H, W) + 8 * B * H * W bytes.
+int ht_reward_delta_f64(const double *h, const double *other, const double *c, int B, int H, int W,
+                        const double *k, int ks, const double *w, int wsz, double w_s, double c1, double c2,
+                        double gain, double *delta_out, void *ws, int64_t ws_bytes, void *stream) {
+  HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty batch");
+  HT_REQUIRE(ks % 2 == 1 && ks <= ht::RMAXK && wsz % 2 == 1 && wsz <= ht::RMAXK,
+             "stencils must be odd and at most %d wide", ht::RMAXK);
+  int64_t need = 0;
+  ht_reward_workspace_bytes(B, H, W, &need);
+  HT_REQUIRE(ws_bytes >= need + 8 * (int64_t)B * H * W, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  double *maps = (double *)ws;
+  double *sums = maps + (size_t)B * ht::NMAPS * H * W;
+  double *m = (double *)((char *)ws + need);
+  HT_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * 2 * B, st));
+  dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
+  ht::reward_maps_kernel<double><<<grid, 256, 0, st>>>(h, nullptr, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s, 1,
+                                                       m, maps, sums, nullptr);
+  ht::reward_le_kernel<double, double><<<grid, 256, 0, st>>>(m, h, other, c, H, W, k, ks, w, wsz, c1, c2, w_s,
+                                                             1.0, 1, 2, maps, delta_out);
+  ht::count_launch(2);
+  HT_CHECK_LAUNCH();
+  return HT_OK;
 }
 
 // REINFORCE (rl.py:132-136): signal = -dlogpi(p, h) (R_b - baseline) * scale,

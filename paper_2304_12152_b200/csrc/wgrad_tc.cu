@@ -416,11 +416,7 @@ template <int NP>
 static int launch(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, cudaStream_t st) {
   using L = Lay<NP>;
   static_assert(L::SMEM <= 232448, "shared memory exceeded");
-  static bool attr = false;
-  if (!attr) {
-    HT_CUDA(cudaFuncSetAttribute(wgrad_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
-    attr = true;
-  }
+  if (int rc = ensure_smem_attr((const void *)wgrad_tc_kernel<NP>, L::SMEM)) return rc;
   if (B <= 0 || H <= 0 || W <= 0) return HT_OK;
   int dev = 0, n_sm = 148;
   HT_CUDA(cudaGetDevice(&dev));

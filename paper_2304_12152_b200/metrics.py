@@ -1,11 +1,12 @@
 """Reward machinery on the GPU -- htlab.metrics drop-in for the training path.
 
-Mirrors MetricConfig (metrics.py:31-39), reward()/RewardContext
-(metrics.py:158-209, region="full") and delta_map (metrics.py:333-392) for
-binary halftones.  All maps are computed by the K3/K4 CUDA kernels
-(csrc/reward.cu) in float64.  The 'valid' evaluation region and non-binary
-edits (multitone) are reporting paths outside the hot path (SURVEY.md §2
-rows 13, 16) and raise NotImplementedError.
+Mirrors MetricConfig (metrics.py:31-39), SsimMaps (metrics.py:110-115),
+reward()/RewardContext (metrics.py:158-209, region="full") and delta_map
+(metrics.py:333-392).  All maps are computed by the K3/K4 CUDA kernels
+(csrc/reward.cu) in float64 from the caller's float64 arrays; the training
+path (reward_signal_device) feeds float32 action / contone maps.  The
+'valid' evaluation region is a reporting path outside the hot path (SURVEY.md
+§2 row 13) and raises NotImplementedError.
 """
 
 import functools
@@ -100,12 +101,25 @@ def reinforce_signal_device(p, m, reward_b, baseline, scale=1.0):
     return out
 
 
+@dataclass
+class SsimMaps:
+    """metrics.py:110-115."""
+    ssim: np.ndarray
+    luminance: np.ndarray
+    contrast: np.ndarray
+    structure: np.ndarray
+
+
 class RewardContext:
     """metrics.RewardContext for region='full' (metrics.py:165-204).
 
-    h is any action map (binary or on an L-level lattice).  .reward is the
-    scalar R = -HVS-MSE + w_s * CSSIM (metrics.py:201-203); delta_map()
-    evaluates substitutions on the GPU (K3 maps + K4 deltas)."""
+    h is any action map (binary or on an L-level lattice), c the contone,
+    both kept float64.  Every map of the reference context is computed on
+    the GPU in float64 (ht_reward_context_f64): f_c, mu_c, scc, sigma_c
+    (contone side), f_h, e, sq_err, mu_h, shh, shc, ssim_maps, cssim_map,
+    reward_map, and the scalars mse, cssim_scalar and reward = -mse + w_s *
+    cssim_scalar (metrics.py:201-203).  delta() evaluates substitutions on
+    the GPU in float64 (K3 maps + K4 deltas)."""
 
     def __init__(self, h, c, cfg, region="full"):
         if region != "full":
@@ -114,30 +128,65 @@ class RewardContext:
                                           "GPU hot path (use region='full')")
             raise ValueError(f"unknown region {region!r}")
         self.cfg, self.region = cfg, region
-        self.h = np.asarray(h, dtype=np.float64).copy()
         self.c = np.asarray(c, dtype=np.float64)
+        self.h = np.asarray(h, dtype=np.float64).copy()
         if self.c.shape != self.h.shape:
             raise ValueError("halftone and contone shapes differ")
-        hh, ww = self.h.shape
-        self.n_region = hh * ww
-        _, _, rew = reward_signal_device(*self._dev(), self.cfg, want_signal=False)
-        self.reward = float(rew[0].item())
-        self.eval_count = 1
+        if self.h.ndim != 2 or self.h.size == 0:
+            raise ValueError("expects non-empty 2-D maps")
+        self.kernel = hvs.build_kernel(cfg.hvs)
+        self.kf = self.kernel.weights[::-1, ::-1].copy()   # _corr_stencil (metrics.py:52-55)
+        self.w = _window_np(cfg.ssim_window, cfg.ssim_sigma)
+        self.mask = np.ones(self.h.shape, dtype=bool)
+        self.n_region = self.h.size
+        self.eval_count = 0
+        self._rebuild()
 
-    def _dev(self):
+    def _rebuild(self):
+        """metrics.py:188-204, on the GPU in float64."""
         import torch
         _lib.require_cuda()
         dev = torch.device("cuda", torch.cuda.current_device())
-        hd = torch.from_numpy(self.h.astype(np.float32))[None].to(dev)
-        cd = torch.from_numpy(self.c.astype(np.float32))[None].to(dev)
-        return hd, None, cd
+        H, W = self.h.shape
+        k, w = stencils_device(self.cfg, dev)
+        hd = torch.from_numpy(self.h)[None].to(dev)
+        cd = torch.from_numpy(self.c)[None].to(dev)
+        maps = torch.empty((1, 8, H, W), dtype=torch.float64, device=dev)
+        extra = torch.empty((1, 7, H, W), dtype=torch.float64, device=dev)
+        sums = torch.empty((1, 2), dtype=torch.float64, device=dev)
+        scratch = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+        cfg = self.cfg
+        _lib.call("ht_reward_context_f64", _lib.ptr(hd), _lib.ptr(cd), 1, H, W, _lib.ptr(k), k.shape[0],
+                  _lib.ptr(w), w.shape[0], float(cfg.w_s), float(cfg.c1), float(cfg.c2),
+                  float(cfg.contrast_gain), _lib.ptr(maps), _lib.ptr(extra), _lib.ptr(sums),
+                  _lib.ptr(scratch), _lib.stream_ptr())
+        m, x, s = maps[0].cpu().numpy(), extra[0].cpu().numpy(), sums[0].cpu().numpy()
+        self.e, self.mu_h, self.shc, self.mu_c, self.scc, self.sigma_c, ssim, self.shh = m
+        self.f_h, self.f_c, lum, con, struct, self.cssim_map, self.reward_map = x
+        self.sq_err = self.e * self.e
+        self.ssim_maps = SsimMaps(ssim, lum, con, struct)
+        self.mse = float(s[0] / self.n_region)
+        self.cssim_scalar = float(s[1] / self.n_region)
+        self.reward = -self.mse + cfg.w_s * self.cssim_scalar
+        self.eval_count += 1
 
     def delta(self, other):
+        """R(h with pixel a -> other[a]) - R(h) for every pixel a (float64)."""
         import torch
-        hd, _, cd = self._dev()
-        od = torch.from_numpy(np.asarray(other, dtype=np.float32))[None].to(hd.device)
-        _, d, _ = reward_signal_device(hd, None, cd, self.cfg, estimator="delta", other=od)
-        return d[0].double().cpu().numpy()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        H, W = self.h.shape
+        k, w = stencils_device(self.cfg, dev)
+        hd = torch.from_numpy(self.h)[None].to(dev)
+        cd = torch.from_numpy(self.c)[None].to(dev)
+        od = torch.from_numpy(np.ascontiguousarray(other, dtype=np.float64))[None].to(dev)
+        out = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+        nbytes = _lib.out_i64("ht_reward_workspace_bytes", 1, H, W) + 8 * H * W
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        cfg = self.cfg
+        _lib.call("ht_reward_delta_f64", _lib.ptr(hd), _lib.ptr(od), _lib.ptr(cd), 1, H, W, _lib.ptr(k),
+                  k.shape[0], _lib.ptr(w), w.shape[0], float(cfg.w_s), float(cfg.c1), float(cfg.c2),
+                  float(cfg.contrast_gain), _lib.ptr(out), _lib.ptr(ws), nbytes, _lib.stream_ptr())
+        return out[0].cpu().numpy()
 
 
 def reward(h, c, cfg=None, region="full"):

@@ -10,9 +10,13 @@ values change, and device-side updates (GPU Adam in rl.train_step) are
 written back to the host arrays.
 
 Compute:
-  forward / backward   fp32 SIMT CUDA kernels, activations kept on the
-                       device between the two calls (nn.py:138-160)
+  forward / backward   training kernels (tcgen05 split-bf16 32->32 convs,
+                       fp32 edge convs), activations kept on the device
+                       between the two calls (nn.py:138-160)
   halftone_device      the fused tcgen05 kernel K1 (inference hot path)
+  Conv2d / ResidualBlock .forward / .backward, and PolicyNetwork with
+  in_channels != 2: the reference's layer-level API, float64 device convs
+  (csrc/conv_f64.cu) chained on the device
 """
 
 import math
@@ -34,16 +38,73 @@ class Parameter:
         self.grad = np.zeros_like(self.value)
 
 
+def _torch():
+    import torch
+    return torch
+
+
+def _dev64(a):
+    """numpy -> float64 CUDA tensor (CUDA tensors pass through as float64)."""
+    torch = _torch()
+    _lib.require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
 class Conv2d:
-    """Parameter container of a 3x3 / stride 1 / zero-pad 1 conv (nn.py:36-80)."""
+    """3x3, stride 1, zero-pad 1 cross-correlation (nn.py:36-80).  forward
+    caches its input (on the device) for backward, which accumulates
+    .weight.grad / .bias.grad and returns dL/dx; both run in float64 on the
+    device (ht_conv3x3_f64, ht_conv3x3_f64_backward)."""
 
     def __init__(self, c_in, c_out):
         self.c_in, self.c_out = c_in, c_out
         self.weight = Parameter(np.zeros((c_out, c_in, 3, 3)))
         self.bias = Parameter(np.zeros(c_out))
+        self._x = None
 
     def params(self):
         return [self.weight, self.bias]
+
+    def forward(self, x):
+        return self._fwd(_dev64(x)).cpu().numpy()
+
+    def backward(self, dout):
+        return self._bwd(_dev64(dout)).cpu().numpy()
+
+    def _fwd(self, xd):
+        torch = _torch()
+        if xd.dim() != 4:
+            raise ValueError("input must be (batch, channels, height, width)")
+        b, c, hgt, wid = xd.shape
+        if c != self.c_in:
+            raise ValueError(f"expected {self.c_in} input channels, got {c}")
+        w, bias = _dev64(self.weight.value), _dev64(self.bias.value)
+        out = torch.empty((b, self.c_out, hgt, wid), dtype=torch.float64, device=xd.device)
+        if out.numel():
+            _lib.call("ht_conv3x3_f64", _lib.ptr(xd), b, c, self.c_out, hgt, wid, _lib.ptr(w),
+                      _lib.ptr(bias), _lib.ptr(out), _lib.stream_ptr())
+        self._x, self._w = xd, w
+        return out
+
+    def _bwd(self, dd):
+        torch = _torch()
+        if self._x is None:
+            raise RuntimeError("backward() needs a preceding forward()")
+        xd, w = self._x, self._w
+        b, c, hgt, wid = xd.shape
+        if tuple(dd.shape) != (b, self.c_out, hgt, wid):
+            raise ValueError("dout shape does not match the last forward")
+        dw = torch.zeros_like(w)
+        db = torch.zeros(self.c_out, dtype=torch.float64, device=xd.device)
+        dx = torch.empty_like(xd)
+        if dx.numel():
+            _lib.call("ht_conv3x3_f64_backward", _lib.ptr(xd), _lib.ptr(dd), b, c, self.c_out, hgt, wid,
+                      _lib.ptr(w), _lib.ptr(dw), _lib.ptr(db), _lib.ptr(dx), _lib.stream_ptr())
+        self.weight.grad += dw.cpu().numpy()
+        self.bias.grad += db.cpu().numpy()
+        return dx
 
 
 class ResidualBlock:
@@ -52,24 +113,33 @@ class ResidualBlock:
     def __init__(self, channels):
         self.conv1 = Conv2d(channels, channels)
         self.conv2 = Conv2d(channels, channels)
+        self._mask = None
 
     def params(self):
         return self.conv1.params() + self.conv2.params()
 
+    def forward(self, x):
+        return self._fwd(_dev64(x)).cpu().numpy()
 
-def _torch():
-    import torch
-    return torch
+    def backward(self, dout):
+        return self._bwd(_dev64(dout)).cpu().numpy()
+
+    def _fwd(self, xd):
+        y = self.conv1._fwd(xd)
+        self._mask = y > 0
+        return xd + self.conv2._fwd(y * self._mask)
+
+    def _bwd(self, dd):
+        dy = self.conv2._bwd(dd) * self._mask
+        return dd + self.conv1._bwd(dy)
 
 
 class PolicyNetwork:
     """Input conv (2 -> C), B residual blocks, output conv (C -> 1), sigmoid."""
 
     def __init__(self, channels=32, blocks=16, in_channels=2):
-        if in_channels != 2:
-            raise ValueError("the policy network takes (contone, noise): in_channels must be 2")
-        if channels < 1 or blocks < 0:
-            raise ValueError("channels must be positive and blocks non-negative")
+        if channels < 1 or blocks < 0 or in_channels < 1:
+            raise ValueError("channels / in_channels must be positive and blocks non-negative")
         self.channels, self.blocks, self.in_channels = channels, blocks, in_channels
         self.conv_in = Conv2d(in_channels, channels)
         self.res = [ResidualBlock(channels) for _ in range(blocks)]
@@ -147,6 +217,10 @@ class PolicyNetwork:
         """Upload + repack if the host parameter values changed; True if it
         uploaded."""
         torch = _torch()
+        if self.in_channels != 2:
+            raise ValueError("the fused / training kernels take the (contone, noise) pair: "
+                             "in_channels must be 2 (other networks run forward/backward "
+                             "layer by layer)")
         if (not force and self._flat is not None and self._uploaded is not None
                 and self._host_matches_upload()):
             return False
@@ -209,6 +283,8 @@ class PolicyNetwork:
             raise ValueError("input must be (batch, channels, height, width)")
         if x.shape[1] != self.in_channels:
             raise ValueError(f"expected {self.in_channels} input channels, got {x.shape[1]}")
+        if self.in_channels != 2:
+            return self._module_forward(x)
         xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(self.device)
         p = self.forward_device(xd)
         return p.double().cpu().numpy()[:, None]
@@ -243,9 +319,32 @@ class PolicyNetwork:
         self._cache = (x, act, p, B, H, W)
         return p
 
+    def _module_forward(self, x):
+        """nn.py:138-150 layer by layer (float64 device convs): the path for
+        networks whose input is not the (contone, noise) pair."""
+        torch = _torch()
+        y = self.conv_in._fwd(_dev64(x))
+        for blk in self.res:
+            y = blk._fwd(y)
+        logits = self.conv_out._fwd(y)
+        if not bool(torch.isfinite(logits).all()):
+            raise FloatingPointError("non-finite logits")
+        p = 1.0 / (1.0 + torch.exp(-logits))
+        self._cache = ("module", p)
+        return p.cpu().numpy()
+
+    def _module_backward(self, dp):
+        p = self._cache[1]
+        dy = self.conv_out._bwd(_dev64(dp).reshape(p.shape) * p * (1.0 - p))
+        for blk in reversed(self.res):
+            dy = blk._bwd(dy)
+        return self.conv_in._bwd(dy).cpu().numpy()
+
     def backward(self, dp):
         """nn.py:152-160: accumulate parameter grads into .grad, return dL/dx."""
         torch = _torch()
+        if self._cache is not None and isinstance(self._cache[0], str):
+            return self._module_backward(dp)
         if self._cache is None:
             raise RuntimeError("backward() needs a preceding forward()")
         x, act, p, B, H, W = self._cache

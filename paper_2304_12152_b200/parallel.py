@@ -39,8 +39,15 @@ class RowStrip:
         return (height, self.in_row0, self.out_row0, self.out_rows)
 
 
+def receptive_radius(blocks):
+    """Receptive-field radius of a PolicyNetwork with `blocks` residual
+    blocks: 2*blocks + 2 stacked 3x3 convs (34 for the paper network)."""
+    return 2 * blocks + 2
+
+
 def row_strip(height, rank, world, halo=RECEPTIVE_RADIUS):
-    """Row strip of `rank` for a page of `height` rows split over `world` ranks."""
+    """Row strip of `rank` for a page of `height` rows split over `world`
+    ranks (halo = the network's receptive_radius)."""
     o0, o1 = shard_range(height, rank, world)
     i0, i1 = max(0, o0 - halo), min(height, o1 + halo)
     return RowStrip(i0, i1 - i0, o0, o1 - o0)
@@ -83,7 +90,7 @@ def halftone_page_strip(net, page, noise, group=None, output="h"):
     import torch
     rank, world = dist_info(group)
     H, W = page.shape
-    st = row_strip(H, rank, world)
+    st = row_strip(H, rank, world, halo=receptive_radius(net.blocks))
     dev = net.device
     c = torch.from_numpy(np.ascontiguousarray(page[st.in_row0:st.in_row0 + st.in_rows],
                                               dtype=np.float32)).to(dev)[None]

@@ -368,6 +368,12 @@ def _dataset_key(dataset):
                   for a in dataset))
 
 
+def reset_prefetch():
+    """Drop the prefetched next-step batch and any queued speculative forward
+    (frees their device buffers; the next train_step draws afresh)."""
+    _next_step.clear()
+
+
 def _take_prepared(dataset, cfg, rng, dev, rank, world):
     key = (_dataset_key(dataset), cfg, str(dev), rank, world)
     prep = _next_step.pop("prep", None)
@@ -387,7 +393,9 @@ def _speculate_forward(net, dev):
     prep = _next_step.get("prep")
     if prep is None or not prep["inputs"]:
         return
-    own = net._cache
+    # this step's backward has consumed the training cache: free it before the
+    # speculative forward allocates its own (no doubled activation memory)
+    net._cache = None
     ins = prep["inputs"]
     x = ins[0] if len(ins) == 1 else torch.cat(ins)
     flag = torch.zeros(max(prep["nm"] + prep["ng"], 1), dtype=torch.int32, device=dev)
@@ -395,7 +403,7 @@ def _speculate_forward(net, dev):
     # Adam's update, which the pull now under way brings to the host)
     p = net.forward_device(x.contiguous(), flag=flag, _sync=False)
     _next_step["spec"] = {"prep": prep, "net": net, "p": p, "flag": flag, "cache": net._cache}
-    net._cache = own
+    net._cache = None
 
 
 def _prefetch_next(dataset, cfg, rng, dev, rank, world):
@@ -415,9 +423,12 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     batch (from a copy of the RNG stream) while the GPU runs this one; the
     next call uses it only if its RNG is exactly where this step left it and
     the dataset holds the same arrays (pass prefetch=False if image contents
-    are edited in place between steps)."""
+    are edited in place between steps: the batch is then always drawn
+    afresh, and nothing is prepared ahead)."""
     torch = _torch()
     _lib.require_cuda()
+    if not prefetch:
+        _next_step.clear()
     rank, world = _dist_info(group)
     dev = net.device
     bs = cfg.batch_size
@@ -429,9 +440,9 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     size = cfg.crop_size
     run_aniso = cfg.w_a != 0.0 and (cfg.levels == 2 or cfg.multitone_anisotropy)
     grad = torch.zeros(net.num_params(), dtype=torch.float64, device=dev)
-    # reward, bin_gap, l_as sums, non-finite flags (one all-reduce, one
-    # read-back per step)
-    stats = torch.zeros(4, dtype=torch.float64, device=dev)
+    # reward, bin_gap, l_as sums, non-finite flags of the MARL and of the
+    # gray forward (one all-reduce, one read-back per step)
+    stats = torch.zeros(5, dtype=torch.float64, device=dev)
     # one forward + one backward over this rank's MARL crops and gray images
     # (the reference's two forwards, batched: samples are independent and the
     # parameters do not change in between); sample b's non-finite flag
@@ -482,14 +493,22 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
         net.backward_device(dps[0] if len(dps) == 1 else torch.cat(dps), grad)
     if prefetch:
         _prefetch_next(dataset, cfg, rng, dev, rank, world)
-    stats[3] = (nonfinite[:nm].amax().double() if nm else 0.0) + \
-        2.0 * (nonfinite[nm:nm + ng].amax().double() if ng else 0.0)
-    allreduce_sum_(grad, stats, group=group)   # the step's one exchange
+    if nm:
+        stats[3] = nonfinite[:nm].amax().double()
+    if ng:
+        stats[4] = nonfinite[nm:nm + ng].amax().double()
+    # the step's one exchange: gradients in fp32 (1.19 MB),
+    # the five statistics in fp64
+    g_ex = grad.float() if world > 1 else grad
+    allreduce_sum_(g_ex, stats, group=group)
+    if g_ex is not grad:
+        grad.copy_(g_ex)
     st = stats.cpu().numpy()
-    if st[3] != 0.0:
-        # first forward with a non-finite logit on any rank; parameters and
-        # Adam state untouched, RNG as the reference leaves it when it raises
-        which = 0 if int(st[3]) % 2 == 1 else 1
+    if st[3] != 0.0 or st[4] != 0.0:
+        # first forward with a non-finite logit on any rank (the MARL forward
+        # comes first); parameters and Adam state untouched, RNG as the
+        # reference leaves it when it raises
+        which = 0 if st[3] != 0.0 else 1
         rng.set_state_words(rng_at_fwd[which])
         raise FloatingPointError("non-finite logits")
     mean_reward = float(st[0] / bs)
@@ -516,10 +535,11 @@ def _part_cache(size):
     return _parts[size]
 
 
-def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None):
+def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None, prefetch=True):
     """rl.py:281-303.  resume_path restores parameters, Adam state, the
     iteration counter and the RNG state words, so a split run reproduces an
-    unsplit one."""
+    unsplit one.  prefetch=False: every step draws its batch afresh (for
+    on_iteration callbacks that edit dataset arrays in place)."""
     cfg.validate()
     if not dataset:
         raise ValueError("dataset is empty")
@@ -532,10 +552,13 @@ def train_loop(cfg, dataset, resume_path=None, on_iteration=None, group=None):
         meta = load_checkpoint(resume_path, net, adam)
         start = meta["iteration"]
         rng.set_state_words(meta["rng_state"])
-    for t in range(start, cfg.iterations):
-        diag = train_step(net, adam, dataset, cfg, rng, t, group=group)
-        if on_iteration is not None:
-            on_iteration(t, diag, net, adam, rng)
+    try:
+        for t in range(start, cfg.iterations):
+            diag = train_step(net, adam, dataset, cfg, rng, t, group=group, prefetch=prefetch)
+            if on_iteration is not None:
+                on_iteration(t, diag, net, adam, rng)
+    finally:
+        reset_prefetch()
     adam.pull_state()
     return net, adam, rng
 

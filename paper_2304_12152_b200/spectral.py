@@ -1,9 +1,12 @@
 """Blue-noise spectral statistics on the GPU -- htlab.spectral drop-in.
 
 ring_partition (spectral.py:39-55) is host-side integer set-up (cached, like
-the reference's _part_cache, rl.py:266-268).  The anisotropy loss, its
-gradient (spectral.py:100-133) and the per-level RAPSD / anisotropy of
-halftones (spectral.py:17-24, 74-97) run in csrc/spectral.cu in float64.
+the reference's _part_cache, rl.py:266-268).  The periodogram, the anisotropy
+loss, its gradient (spectral.py:17-24, 100-133) and the RAPSD / anisotropy of
+halftones (spectral.py:74-97) run in csrc/spectral.cu in float64 (batched
+cuFFT transforms + ring-reduction kernels).  The drop-in functions take the
+reference's float64 arrays and compute on them in float64; the training path
+feeds float32 probability maps (anisotropy_device).
 """
 
 import math
@@ -80,25 +83,56 @@ def anisotropy_device(x, part=None, scale=1.0, want_grad=True):
     return loss, grad
 
 
-def _to_device(x):
+def _to_device(x, what="expects"):
+    """float64 (1, H, W) CUDA tensor of a non-empty 2-D array (no downcast)."""
     import torch
     _lib.require_cuda()
     x = np.asarray(x, dtype=np.float64)
     if x.ndim != 2 or x.size == 0:
-        raise ValueError("expects a non-empty 2-D array")
-    return torch.from_numpy(x.astype(np.float32))[None].cuda()
+        raise ValueError(f"{what} a non-empty 2-D array")
+    return torch.from_numpy(np.ascontiguousarray(x))[None].cuda()
+
+
+def _aniso_f64(xd, part, want_grad):
+    import torch
+    B, H, W = xd.shape
+    part = part or ring_partition((H, W))
+    if part.shape != (H, W):
+        raise ValueError("partition shape mismatch")
+    ring, counts = _part_device(part, xd.device)
+    nr = len(part.radii)
+    loss = torch.empty(B, dtype=torch.float64, device=xd.device)
+    grad = torch.empty((B, H, W), dtype=torch.float64, device=xd.device) if want_grad else None
+    nbytes = _lib.out_i64("ht_spectral_workspace_bytes", B, H, W, nr)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=xd.device)
+    _lib.call("ht_anisotropy_f64", _lib.ptr(xd), B, H, W, _lib.ptr(ring), _lib.ptr(counts), nr, 1.0,
+              _lib.ptr(loss), _lib.ptr(grad), _lib.ptr(ws), nbytes, _lib.stream_ptr())
+    return loss, grad
 
 
 def anisotropy_loss(x, part=None):
-    """spectral.py:117-121."""
-    loss, _ = anisotropy_device(_to_device(x), part, want_grad=False)
+    """spectral.py:117-121 (float64 throughout)."""
+    loss, _ = _aniso_f64(_to_device(x), part, want_grad=False)
     return float(loss[0].item())
 
 
 def anisotropy_loss_backward(x, part=None):
     """spectral.py:124-133: analytic gradient (float64 array)."""
-    _, grad = anisotropy_device(_to_device(x), part)
-    return grad[0].double().cpu().numpy()
+    _, grad = _aniso_f64(_to_device(x), part, want_grad=True)
+    return grad[0].cpu().numpy()
+
+
+def periodogram(x):
+    """spectral.py:17-24: P(f) = |DFT(x)|^2 / N, float64 (H, W)."""
+    import torch
+    xd = _to_device(x, "periodogram expects")
+    _, H, W = xd.shape
+    P = torch.empty((1, H, W), dtype=torch.float64, device=xd.device)
+    nbytes = _lib.out_i64("ht_spectral_workspace_bytes", 1, H, W, 1)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=xd.device)
+    _lib.call("ht_periodogram_f64", _lib.ptr(xd), 1, H, W, _lib.ptr(P), _lib.ptr(ws), nbytes,
+              _lib.stream_ptr())
+    return P[0].cpu().numpy()
 
 
 @dataclass
@@ -130,11 +164,48 @@ def rapsd_device(x, part=None):
     return power, anis, dc
 
 
+def rapsd(p_hat, part=None):
+    """spectral.py:74-88: radially averaged power and per-ring anisotropy of
+    a periodogram p_hat (H, W) -> RapsdCurve."""
+    import torch
+    _lib.require_cuda()
+    p_hat = np.asarray(p_hat, dtype=np.float64)
+    if p_hat.ndim != 2 or p_hat.size == 0:
+        raise ValueError("rapsd expects a non-empty 2-D periodogram")
+    part = part or ring_partition(p_hat.shape)
+    if part.shape != p_hat.shape:
+        raise ValueError("partition shape mismatch")
+    H, W = p_hat.shape
+    Pd = torch.from_numpy(np.ascontiguousarray(p_hat))[None].cuda()
+    ring, counts = _part_device(part, Pd.device)
+    nr = len(part.radii)
+    power = torch.empty((1, nr), dtype=torch.float64, device=Pd.device)
+    anis = torch.empty((1, nr), dtype=torch.float64, device=Pd.device)
+    dc = torch.empty(1, dtype=torch.float64, device=Pd.device)
+    nbytes = _lib.out_i64("ht_spectral_workspace_bytes", 1, H, W, nr)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=Pd.device)
+    _lib.call("ht_rapsd_power_f64", _lib.ptr(Pd), 1, H, W, _lib.ptr(ring), _lib.ptr(counts), nr,
+              _lib.ptr(power), _lib.ptr(anis), _lib.ptr(dc), _lib.ptr(ws), nbytes, _lib.stream_ptr())
+    return RapsdCurve(part.radii.copy(), power[0].cpu().numpy(), anis[0].cpu().numpy(),
+                      part.counts.copy(), float(dc[0].item()))
+
+
 def image_rapsd(x, part=None):
-    """rapsd(periodogram(x)) (spectral.py:17-24, 74-88) for one image."""
+    """rapsd(periodogram(x)) (spectral.py:17-24, 74-88) for one image, in one
+    pass on the device (float64)."""
+    import torch
     xd = _to_device(x)
-    part = part or ring_partition(xd.shape[1:])
-    power, anis, dc = rapsd_device(xd, part)
+    _, H, W = xd.shape
+    part = part or ring_partition((H, W))
+    ring, counts = _part_device(part, xd.device)
+    nr = len(part.radii)
+    power = torch.empty((1, nr), dtype=torch.float64, device=xd.device)
+    anis = torch.empty((1, nr), dtype=torch.float64, device=xd.device)
+    dc = torch.empty(1, dtype=torch.float64, device=xd.device)
+    nbytes = _lib.out_i64("ht_spectral_workspace_bytes", 1, H, W, nr)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=xd.device)
+    _lib.call("ht_rapsd_f64", _lib.ptr(xd), 1, H, W, _lib.ptr(ring), _lib.ptr(counts), nr,
+              _lib.ptr(power), _lib.ptr(anis), _lib.ptr(dc), _lib.ptr(ws), nbytes, _lib.stream_ptr())
     return RapsdCurve(part.radii.copy(), power[0].cpu().numpy(), anis[0].cpu().numpy(),
                       part.counts.copy(), float(dc[0].item()))
 

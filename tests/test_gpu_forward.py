@@ -160,15 +160,54 @@ def test_device_api_without_sync_reuses_packed_weights():
 @pytest.mark.parametrize("nb", [0, 1, 2, 3, 5])
 def test_fused_pass_plans_for_other_depths(nb):
     """Every pass-plan shape of the fused kernel (conv_in-only, conv_out-only,
-    odd block counts) against the fp32 SIMT path on the same net."""
+    odd block counts) against the reference oracle on the same net (and the
+    fp32 SIMT path against it at 2e-5)."""
+    from oracle import htoracle as O
     from paper_2304_12152_b200 import rl, synth
     from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
     net = _net(0.05, 32, nb, seed=nb)
     c = synth.contone(45, 300, seed=nb)
     z = gaussian_noise_map_f32(Rng(nb), 300, 45)
+    params = O.init_params(O.Rng(nb), 32, nb, 2, 0.05)
+    _, p_ref = O.halftone(params, c.astype(np.float64), z.astype(np.float64))
     h0, p0 = rl.halftone(net, c, z, impl=0)
     h1, p1 = rl.halftone(net, c, z, impl=1)
-    _check(p0, h0, p1, P_TOL)
+    _check(p0, h0, p_ref, P_TOL)
+    _check(p1, h1, p_ref, 2e-5)
+
+
+def test_two_networks_on_two_streams_concurrently():
+    """Two networks halftoning at the same time on two streams of one GPU
+    (each pass's biases travel with its launch, so neither sees the other's):
+    the results equal each network's result run alone, bitwise."""
+    import torch
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    nets = [_net(0.05, seed=1), _net(0.05, seed=2)]
+    for n in nets:
+        n.conv_out.bias.value[0] = 0.3 * (1 if n is nets[0] else -1)
+        for blk in n.res:
+            blk.conv2.bias.value[:] = 0.01 * (1 if n is nets[0] else -1)
+    c = torch.from_numpy(np.stack([synth.contone(256, 256, seed=s) for s in range(8)])).cuda()
+    z = torch.from_numpy(np.stack([gaussian_noise_map_f32(Rng(s), 256, 256) for s in range(8)])).cuda()
+    alone = []
+    for n in nets:
+        p = torch.empty_like(c)
+        n.halftone_device(c, z, p_out=p, check=True)
+        alone.append(p.clone())
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in nets]
+    outs = [torch.empty_like(c) for _ in nets]
+    wss = [None, None]
+    for rep in range(4):
+        for k, (n, s) in enumerate(zip(nets, streams)):
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                wss[k] = n.halftone_device(c, z, p_out=outs[k], workspace=wss[k], stream=s)
+        torch.cuda.synchronize()
+        for k in range(2):
+            assert torch.equal(outs[k], alone[k]), f"network {k}, repetition {rep}"
+    assert not torch.equal(alone[0], alone[1])
 
 
 def test_engine_draws_noise_on_device_in_infer_halftone_order():

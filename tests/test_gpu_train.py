@@ -104,6 +104,46 @@ def test_anisotropy_loss_and_grad():
     assert rel(pr @ gr.ravel(), g["x256_grad_probe"]) < 1e-6
 
 
+def test_anisotropy_float64_api_is_float64():
+    """spectral.anisotropy_loss(_backward) on float64 arrays compute in
+    float64 (no float32 round trip): 1e-12 against the reference's goldens."""
+    from paper_2304_12152_b200 import spectral
+    g = golden("spectral.npz")
+    assert abs(spectral.anisotropy_loss(g["x32"]) / g["x32_loss"][0] - 1) < 1e-12
+    assert rel(spectral.anisotropy_loss_backward(g["x32"]), g["x32_grad"]) < 1e-12
+    x = g["x256"].astype(np.float64)
+    assert abs(spectral.anisotropy_loss(x) / g["x256_loss"][0] - 1) < 1e-12
+    gr = spectral.anisotropy_loss_backward(x)
+    assert abs(np.linalg.norm(gr) / g["x256_grad_norm"][0] - 1) < 1e-12
+    assert rel(gr[:16, :16], g["x256_grad_crop"]) < 1e-10
+
+
+def test_periodogram_and_rapsd_of_periodogram():
+    """spectral.periodogram (spectral.py:17-24) and spectral.rapsd(p_hat,
+    part) (spectral.py:74-88) against the reference's rapsd(periodogram(h))
+    and the oracle's periodogram; Parseval sum(P) = sum(x^2)."""
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import spectral
+    g = golden("spectral.npz")
+    P = spectral.periodogram(g["h32"])
+    assert P.dtype == np.float64 and P.shape == (32, 32)
+    assert np.allclose(P, O.periodogram(g["h32"]), rtol=1e-12, atol=1e-12)
+    assert abs(P.sum() - np.sum(g["h32"] ** 2)) < 1e-9
+    part = spectral.ring_partition((32, 32))
+    cur = spectral.rapsd(P, part)
+    assert np.allclose(cur.power, g["h32_power"], rtol=1e-12, atol=0)
+    assert np.allclose(cur.anisotropy, g["h32_anis"], rtol=1e-10, atol=0, equal_nan=True)
+    assert abs(cur.dc_power - g["h32_dc"][0]) < 1e-12
+    assert np.array_equal(cur.radii, part.radii) and np.array_equal(cur.counts, part.counts)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((7, 12))                 # ragged, odd height
+    assert np.allclose(spectral.periodogram(x), O.periodogram(x), rtol=1e-12, atol=1e-12)
+    with pytest.raises(ValueError):
+        spectral.periodogram(np.zeros((0, 4)))
+    with pytest.raises(ValueError):
+        spectral.rapsd(P, spectral.ring_partition((16, 32)))
+
+
 def test_rapsd_of_halftone():
     from paper_2304_12152_b200 import spectral
     g = golden("spectral.npz")
@@ -196,6 +236,73 @@ def test_train_step_nonfinite_raises_before_update():
     assert np.array_equal(net.flat_values(), p0, equal_nan=True)
     assert adam.t == 0
     assert rng.state_words() == expect.state_words()
+
+
+def test_train_step_nonfinite_two_ranks_both_flag_marl(monkeypatch):
+    """Data parallel: when two ranks both see a non-finite MARL logit, the
+    summed flags still name the MARL forward (separate statistics slots), so
+    the RNG is rewound to where the reference's first forward raises."""
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    g = golden("train.npz")
+    cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
+                         anisotropy_batch_size=2, hvs_model="gaussian")
+    ds = list(g["mini_ds"])
+    net = PolicyNetwork(8, 2)
+    rng = Rng(cfg.seed)
+    net.init_params(rng)
+    net.conv_out.bias.value[0] = np.inf
+    expect = Rng(0)
+    expect.set_state_words(rng.state_words())
+    rl.draw_batch(ds, cfg, expect)
+
+    def fake_allreduce(*tensors, group=None):    # a second rank with the same flags
+        for t in tensors:
+            t.mul_(2.0)
+        return tensors
+
+    monkeypatch.setattr(rl, "_dist_info", lambda group=None: (0, 2))
+    monkeypatch.setattr(rl, "allreduce_sum_", fake_allreduce)
+    with pytest.raises(FloatingPointError):
+        rl.train_step(net, Adam(net.params()), ds, cfg, rng, 0, prefetch=False)
+    assert rng.state_words() == expect.state_words()
+
+
+def test_train_step_prefetch_false_draws_afresh():
+    """prefetch=False after a prefetching step: the batch is drawn from the
+    (edited) dataset, not taken from the prepared one."""
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    from paper_2304_12152_b200.nn import Adam, PolicyNetwork
+    g = golden("train.npz")
+    cfg = rl.TrainConfig(iterations=10, batch_size=2, crop_size=24, channels=8, blocks=2,
+                         anisotropy_batch_size=2, hvs_model="gaussian")
+
+    def run(edit):
+        ds = [a.copy() for a in g["mini_ds"]]
+        net = PolicyNetwork(8, 2)
+        adam = Adam(net.params())
+        rng = Rng(cfg.seed)
+        net.init_params(rng)
+        rl.train_step(net, adam, ds, cfg, rng, 0)          # prefetches step 1's batch
+        if edit:
+            for a in ds:
+                a[...] = 1.0 - a                           # in place: same arrays
+        d = rl.train_step(net, adam, ds, cfg, rng, 1, prefetch=False)
+        rl.reset_prefetch()
+        return d["reward"]
+
+    fresh = run(True)
+    rl.reset_prefetch()
+    ds = [1.0 - a for a in g["mini_ds"]]
+    net = PolicyNetwork(8, 2)
+    adam = Adam(net.params())
+    rng = Rng(cfg.seed)
+    net.init_params(rng)
+    rl.train_step(net, adam, [a.copy() for a in g["mini_ds"]], cfg, rng, 0, prefetch=False)
+    want = rl.train_step(net, adam, ds, cfg, rng, 1, prefetch=False)["reward"]
+    assert abs(fresh - want) <= 1e-9 * max(1.0, abs(want))
 
 
 def test_train_step_prefetch_is_transparent():
