@@ -12,6 +12,6 @@ for f in paper_2304_12152_b200/csrc/*.cu; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -cudart static $out/*.o \
-  -o debug/libhtb200_$name.so
+  -L/usr/local/cuda/lib64 -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 -o debug/libhtb200_$name.so
 rm -rf $out
 echo built debug/libhtb200_$name.so
