@@ -411,8 +411,65 @@ class PolicyNetwork:
                       in_rows, out_row0, out_rows, int(levels), _lib.ptr(p_out), _lib.ptr(h_out),
                       _lib.ptr(workspace), nbytes, impl, sp)
         if check:
-            _lib.call("ht_halftone_check", _lib.ptr(workspace), sp)
+            try:
+                _lib.call("ht_halftone_check", _lib.ptr(workspace), sp)
+            except FloatingPointError:
+                # K1 carries activations as fp16 MMA operands: a network whose
+                # activations leave fp16's range (|x| > 65504, e.g. std-0.1
+                # random init: ~1e5 after 16 blocks) overflows there while the
+                # reference (fp64) stays finite -- and at that scale fp32 no
+                # longer resolves p near the logit's zero crossings either.
+                # Redo the batch in float64 on the device (the reference's
+                # precision); it raises only if the logits are non-finite in
+                # float64 too, exactly where the reference raises.
+                self._halftone_f64(c, z, p_out, h_out, pbm_out, rows, levels, stream)
         return workspace
+
+    def _halftone_f64(self, c, z, p_out, h_out, pbm_out, rows, levels, stream):
+        """Float64 device forward + threshold epilogue, image by image, layer
+        by layer (ht_conv3x3_f64; nothing cached for backward)."""
+        torch = _torch()
+        H, in_row0, out_row0, out_rows = rows
+        lo = out_row0 - in_row0
+        W = c.shape[-1]
+        with torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream()):
+            sp = _lib.stream_ptr()
+            convs = [self.conv_in]
+            for blk in self.res:
+                convs += [blk.conv1, blk.conv2]
+            convs.append(self.conv_out)
+            wb = [(_dev64(cv.weight.value), _dev64(cv.bias.value)) for cv in convs]
+
+            def conv(x, k):
+                w, b = wb[k]
+                out = torch.empty((1, w.shape[0], x.shape[2], W), dtype=torch.float64, device=x.device)
+                _lib.call("ht_conv3x3_f64", _lib.ptr(x), 1, x.shape[1], w.shape[0], x.shape[2], W, _lib.ptr(w),
+                          _lib.ptr(b), _lib.ptr(out), sp)
+                return out
+
+            for i in range(c.shape[0]):
+                y = conv(torch.stack((c[i], z[i]))[None].double().contiguous(), 0)
+                for k in range(self.blocks):
+                    y = y + conv(torch.relu(conv(y, 1 + 2 * k)), 2 + 2 * k)
+                logit = conv(y, len(convs) - 1)[0, 0, lo:lo + out_rows]
+                if not bool(torch.isfinite(logit).all()):
+                    raise FloatingPointError("non-finite logits")
+                p = 1.0 / (1.0 + torch.exp(-logit))
+                if p_out is not None:
+                    p_out[i].copy_(p)
+                if levels == 2:
+                    h = (p >= 0.5).to(torch.uint8)
+                else:   # multitone.quantize_multitone (multitone.py:61-67)
+                    s = levels - 1
+                    h = torch.clamp(torch.floor(p * s + 0.5), 0, s).to(torch.uint8)
+                if h_out is not None:
+                    h_out[i].copy_(h)
+                if pbm_out is not None:   # PBM P4: bit 1 = black, MSB first (imagecore.py:289-297)
+                    nb = (W + 7) // 8
+                    bits = torch.zeros((out_rows, nb * 8), dtype=torch.uint8, device=p.device)
+                    bits[:, :W] = 1 - h
+                    wts = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.uint8, device=p.device)
+                    pbm_out[i].copy_((bits.view(out_rows, nb, 8) * wts).sum(-1).to(torch.uint8))
 
 
 class Adam:

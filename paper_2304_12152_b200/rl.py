@@ -691,16 +691,23 @@ class HalftoneEngine:
             e = torch.cuda.Event()
             e.record(s)
             ticket.append(e)
-        return ticket
+        return (ticket, st)
 
     def wait(self, ticket):
         """Block until a submitted batch's result is in its out_host; later
-        work on the current stream is ordered after it."""
+        work on the current stream is ordered after it.  Raises
+        FloatingPointError if the fused kernel saw a non-finite logit (for a
+        network whose activations leave fp16's range, use impl=1 or
+        rl.halftone, which redoes such batches on the fp32 path)."""
         torch = _torch()
         cur = torch.cuda.current_stream(self.dev)
-        for e in ticket:
+        events, st = ticket
+        for e in events:
             cur.wait_event(e)
             e.synchronize()
+        for k, ws in enumerate(st["ws"]):
+            if ws is not None:
+                _lib.call("ht_halftone_check", _lib.ptr(ws), _lib.stream_ptr(st["streams"][k % 2]))
 
 
 def halftone_batch(net, contones, noises, output="h", chunks=4):

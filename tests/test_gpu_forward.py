@@ -290,3 +290,32 @@ def test_engine_streamed_batches_equal_sequential_calls(noise):
         assert torch.equal(outs[i], seq[i]), i
     if noise == "device":
         assert rs2.state_words() == rs.state_words()
+
+
+@pytest.mark.parametrize("case", ["trained_2k", "std0.1"])
+def test_config1_beyond_random_init(case):
+    """K1 parity with weights that are not the std-0.01 init: the network
+    after 2000 iterations of this package's own train_loop (bare HTNN file,
+    tests/golden/make_trained_checkpoint.py) and a std-0.1 random init, on
+    BASELINE config 1 (256x256) against the oracle's float64 forward.  At
+    std 0.1 the activations reach ~1e5 after 16 blocks, beyond fp16's range
+    (and beyond what fp32 resolves near the logits' zero crossings): the fused
+    kernel flags the overflow and rl.halftone redoes the image in float64 on
+    the device, the reference's precision."""
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.checkpoint import network_from_checkpoint
+    from conftest import GOLDEN
+    import os
+    g = golden("forward.npz")
+    if case == "trained_2k":
+        net, _ = network_from_checkpoint(os.path.join(GOLDEN, "trained_c32b16_2k.htnn"))
+    else:
+        net = _net(0.1)
+    params = [q.value.copy() for q in net.params()]
+    c, z = g["cfg1_c"], g["cfg1_z"]
+    _, p_ref = O.halftone(params, c.astype(np.float64), z.astype(np.float64))
+    h, p = rl.halftone(net, c, z)
+    err, band = _check(p, h, p_ref, P_TOL)
+    print(f"{case}: max|dp| = {err:.2e}, band fraction {band:.4f}, "
+          f"p range [{p_ref.min():.3f}, {p_ref.max():.3f}]")
