@@ -210,6 +210,8 @@ struct TcParams {
   float *x_out;         // !HO: (rows, 8, VW, 4) fp32
   float *p;             // HO: (B, out_rows, W) (nullable)
   uint8_t *h;           // HO: (B, out_rows, W) (nullable)
+  uint32_t *pbm;        // HO: PBM P4 payload as words (nullable; zeroed, padded to 4 B)
+  int pbm_rb;           // bytes per PBM row, ceil(W / 8)
   int *flag;            // HO: non-finite logit flag
   int B, W, VW, rows;   // rows = window rows held by the pass buffers
   long long pitch;      // pass-buffer pixels per (row, channel group): x_pitch(VW)
@@ -534,11 +536,29 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
         if (drain) {
           if constexpr (kind == K_OUT) {
             const float logit = vals[0] + PBIAS(j, 0);
-            if (lane_valid && in_img && d >= R0 && d < R1) {
+            const bool px = lane_valid && in_img && d >= R0 && d < R1;
+            if (px) {
               if (!isfinite(logit)) atomicOr(P.flag, 1);
               const size_t o = ((size_t)b * P.out_rows + (d - P.r_lo)) * P.W + col;
               if (P.p) P.p[o] = 1.f / (1.f + __expf(-logit));
               if (P.h) P.h[o] = level_of(logit, P.steps);
+            }
+            if (P.pbm) {
+              // PBM P4 bits straight from the logits (imagecore.py:289-297:
+              // bit = 1 - h = black, MSB first, rows padded to bytes): the
+              // warp's bits are OR-reduced per 32-bit word of the payload
+              // (its 32 columns touch <= 3 words per image row; a strip's
+              // edge word is shared with the neighbouring strip's CTA)
+              uint32_t widx = 0xffffffffu, val = 0u;
+              if (px) {
+                const uint32_t byte =
+                    (uint32_t)(((size_t)b * P.out_rows + (d - P.r_lo)) * P.pbm_rb + (col >> 3));
+                widx = byte >> 2;
+                val = (logit >= 0.f ? 0u : 1u) << (7 - (col & 7) + 8 * (byte & 3));
+              }
+              const unsigned peers = __match_any_sync(0xffffffffu, widx);
+              const uint32_t orv = __reduce_or_sync(peers, val);
+              if (px && orv && lane == __ffs(peers) - 1) atomicOr(P.pbm + widx, orv);
             }
           } else if constexpr (PL::feeds_next(j)) {
             const int q = NABUF == 3 ? slot : (d & 1);   // A buffer of row d
@@ -706,7 +726,7 @@ static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
 
 int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float *z, int B, int H,
         int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p, uint8_t *h,
-        void *ws, int64_t ws_bytes, int *flag_dev, int levels, cudaStream_t st) {
+        uint32_t *pbm_words, void *ws, int64_t ws_bytes, int *flag_dev, int levels, cudaStream_t st) {
   (void)H;
   const int64_t need = workspace_bytes(NB, B, H, W, in_rows);
   HT_REQUIRE(ws_bytes >= need, "workspace too small: %lld < %lld", (long long)ws_bytes, (long long)need);
@@ -747,6 +767,8 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     prm.x_in = in_x;
     prm.x_out = pd.ho ? nullptr : out_x;
     prm.p = p; prm.h = h; prm.flag = flag_dev;
+    prm.pbm = pd.ho ? pbm_words : nullptr;
+    prm.pbm_rb = (W + 7) / 8;
     prm.B = B; prm.W = W; prm.VW = VW; prm.rows = in_rows;
     prm.S = STRIP_S;
     prm.pitch = x_pitch(VW);

@@ -53,7 +53,8 @@ int64_t workspace_bytes(int NB, int B, int H, int W, int in_rows);
 
 int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float *z, int B,
         int H, int W, int in_row0, int in_rows, int out_row0, int out_rows, float *p,
-        uint8_t *h, void *ws, int64_t ws_bytes, int *flag_dev, int levels, cudaStream_t st);
+        uint8_t *h, uint32_t *pbm_words, void *ws, int64_t ws_bytes, int *flag_dev, int levels,
+        cudaStream_t st);
 
 }  // namespace tc
 }  // namespace ht

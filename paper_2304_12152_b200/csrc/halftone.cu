@@ -40,11 +40,11 @@ int ht_halftone_workspace_bytes(int C, int NB, int B, int H, int W, int in_rows,
                                 int impl, int64_t *bytes) {
   if (B < 1 || H < 1 || W < 1 || in_rows < 1) return ht::fail(HT_E_INVALID, "empty image");
   int64_t base = 256;  // flag
-  base += ht::align256((int64_t)B * out_rows * W);  // uint8 h scratch for PBM
-  if (impl == 0 && C == ht::tc::C)
-    *bytes = base + ht::tc::workspace_bytes(NB, B, H, W, in_rows);
-  else
-    *bytes = base + ht::simt_halftone_ws(C, B, W, in_rows);
+  if (impl == 0 && C == ht::tc::C)   // PBM words (K1 writes the payload bits itself)
+    *bytes = base + ht::align256(((int64_t)B * out_rows * ((W + 7) / 8) + 3) / 4 * 4) +
+             ht::tc::workspace_bytes(NB, B, H, W, in_rows);
+  else                               // uint8 h scratch for the PBM pack kernel
+    *bytes = base + ht::align256((int64_t)B * out_rows * W) + ht::simt_halftone_ws(C, B, W, in_rows);
   return HT_OK;
 }
 
@@ -73,20 +73,34 @@ static int halftone_impl(const void *packed, int C, int NB, const float *c, cons
   cudaStream_t st = (cudaStream_t)stream;
   char *wsb = (char *)ws;
   int *flag = (int *)wsb;
+  HT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  const int64_t pbm_bytes = (int64_t)B * out_rows * ((W + 7) / 8);
+  if (impl == 0) {
+    // K1 ORs the PBM bits into 32-bit words: straight into the caller's
+    // buffer when it is word-aligned and whole words long, else into a padded
+    // workspace copy (then one device copy of the exact payload)
+    HT_REQUIRE(pbm_bytes < (1ll << 34), "PBM payload too large");
+    uint32_t *words = (uint32_t *)(wsb + 256);
+    const bool direct = pbm && ((uintptr_t)pbm % 4 == 0) && pbm_bytes % 4 == 0;
+    if (direct) words = (uint32_t *)pbm;
+    const int64_t wbytes = (pbm_bytes + 3) / 4 * 4;
+    char *rest = wsb + 256 + ht::align256(wbytes);
+    const int64_t rest_bytes = ws_bytes - (rest - wsb);
+    if (pbm) HT_CUDA(cudaMemsetAsync(words, 0, wbytes, st));
+    ht::PackLayout L = ht::pack_layout(C, NB);
+    rc = ht::tc::run((const char *)packed + L.tc_off, (const float *)((const char *)packed + L.tcb_off),
+                     NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p, h, pbm ? words : nullptr,
+                     rest, rest_bytes, flag, levels, st);
+    if (rc) return rc;
+    if (pbm && !direct) HT_CUDA(cudaMemcpyAsync(pbm, words, pbm_bytes, cudaMemcpyDeviceToDevice, st));
+    return HT_OK;
+  }
   uint8_t *hscratch = (uint8_t *)(wsb + 256);
   char *rest = wsb + 256 + ht::align256((int64_t)B * out_rows * W);
   const int64_t rest_bytes = ws_bytes - (rest - wsb);
-  HT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
   uint8_t *hout = h ? h : (pbm ? hscratch : nullptr);
-  if (impl == 0) {
-    ht::PackLayout L = ht::pack_layout(C, NB);
-    rc = ht::tc::run((const char *)packed + L.tc_off, (const float *)((const char *)packed + L.tcb_off),
-                     NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p, hout, rest,
-                     rest_bytes, flag, levels, st);
-  } else {
-    rc = ht::simt_halftone(packed, C, NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p,
-                           hout, rest, rest_bytes, flag, levels, st);
-  }
+  rc = ht::simt_halftone(packed, C, NB, c, z, B, H, W, in_row0, in_rows, out_row0, out_rows, p,
+                         hout, rest, rest_bytes, flag, levels, st);
   if (rc) return rc;
   if (pbm) {
     const int64_t n = (int64_t)B * out_rows * ((W + 7) / 8);

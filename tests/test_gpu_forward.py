@@ -109,20 +109,36 @@ def test_row_window_sharding_bitwise():
     assert torch.equal(stitched, full)
 
 
-def test_pbm_payload_matches_packbits():
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("B,H,W", [(1, 33, 77), (3, 20, 130), (5, 17, 256), (2, 9, 1)])
+def test_pbm_payload_matches_packbits(impl, B, H, W):
+    """The PBM P4 payload (imagecore.py:289-297) written by the fused kernel's
+    epilogue (impl 0: bits OR-reduced per word straight from the logits; a
+    word can span two strips' CTAs) or packed from h (impl 1) equals
+    np.packbits(1 - h) -- for payloads that are whole words (written in
+    place) and ragged ones (padded scratch + copy), with and without h."""
     import torch
     from paper_2304_12152_b200 import synth
     from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
     net = _net(0.05)
-    H, W = 33, 77
-    c = torch.from_numpy(synth.contone(H, W, seed=2)).cuda()[None]
-    z = torch.from_numpy(gaussian_noise_map_f32(Rng(2), W, H)).cuda()[None]
-    h = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
-    pbm = torch.empty((1, H, (W + 7) // 8), dtype=torch.uint8, device="cuda")
-    net.halftone_device(c, z, h_out=h, pbm_out=pbm)
-    hh = h.cpu().numpy()[0]
-    want = np.packbits((1 - hh).astype(np.uint8), axis=1)     # imagecore.py:293-294
-    assert np.array_equal(pbm.cpu().numpy()[0], want)
+    c = torch.from_numpy(np.stack([synth.contone(H, W, seed=2 + i) for i in range(B)])).cuda()
+    z = torch.from_numpy(np.stack([gaussian_noise_map_f32(Rng(2 + i), W, H) for i in range(B)])).cuda()
+    h = torch.empty((B, H, W), dtype=torch.uint8, device="cuda")
+    pbm = torch.full((B, H, (W + 7) // 8), 0xAB, dtype=torch.uint8, device="cuda")
+    net.halftone_device(c, z, h_out=h, pbm_out=pbm, impl=impl, check=True)
+    want = np.packbits((1 - h.cpu().numpy()).astype(np.uint8), axis=2)     # imagecore.py:293-294
+    assert np.array_equal(pbm.cpu().numpy(), want)
+    pbm2 = torch.full_like(pbm, 0x5C)
+    net.halftone_device(c, z, pbm_out=pbm2, impl=impl, check=True)     # payload only
+    assert torch.equal(pbm2, pbm)
+    # a window of rows (row-strip sharding), odd offset
+    if H > 4:
+        rows = (H, 1, 2, H - 3)
+        pw = torch.zeros((B, H - 3, (W + 7) // 8), dtype=torch.uint8, device="cuda")
+        hw = torch.empty((B, H - 3, W), dtype=torch.uint8, device="cuda")
+        net.halftone_device(c[:, 1:], z[:, 1:], h_out=hw, pbm_out=pw, rows=rows, impl=impl, check=True)
+        assert np.array_equal(pw.cpu().numpy(),
+                              np.packbits((1 - hw.cpu().numpy()).astype(np.uint8), axis=2))
 
 
 def test_nonfinite_logits_raise():
