@@ -514,10 +514,19 @@ def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
     from paper_2304_12152_b200.parallel import shard_range
+    # HT_BENCH_FUNCTIONAL=1: control-flow check of the N-rank path on fewer
+    # GPUs (ranks share devices, gloo instead of NCCL); its numbers are not
+    # measurements and the line says so
+    functional = os.environ.get("HT_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2304_12152_b200 import _lib, rl
     D = Dist(rank, world, dev)
     burst, sustained, hbm, src = load_peaks()
@@ -653,6 +662,8 @@ def run_ours(args, rank, world, local):
             out["weak_scaling"] = weak
         if configs:
             out["configs"] = configs
+        if functional:
+            out["functional_check_only"] = "ranks shared GPUs over gloo: not a measurement"
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -702,6 +713,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import torch
+        if torch.cuda.device_count() < args.gpus and os.environ.get("HT_BENCH_FUNCTIONAL") != "1":
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but {torch.cuda.device_count()} GPU(s) visible")
         sys.exit(relaunch(args))
     rank, world, local = dist_setup(args)
     if args.impl == "reference":
