@@ -140,8 +140,10 @@ int ht_timing_read(int *tags, float *ms, int max, int *count);
  * split-bf16 operands (default), 1 = fp32 SIMT kernels only (cross-check).
  * Process-wide. */
 int ht_set_train_conv_impl(int impl);
-/* bf16 parts of the tensor-core weight gradient: 3 (six products, fp32
- * level; default) or 2 (three products, ~2^-16 per product). */
+/* bf16 parts of the tensor-core weight gradient: 2 (three products,
+ * ~2^-16 per product; default -- the config-5 step stays at 1.6e-5 of the
+ * reference normwise per tensor, tests/test_gpu_train_cfg5.py) or 3 (six
+ * products, fp32 level). */
 int ht_set_wgrad_parts(int parts);
 /* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
  * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +

@@ -114,7 +114,7 @@ void timing_mark_end(cudaStream_t st) {
 }
 
 int g_train_conv_impl = 0;
-int g_wgrad_parts = 3;
+int g_wgrad_parts = 2;
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
 static inline uint64_t splitmix64(uint64_t &s) {

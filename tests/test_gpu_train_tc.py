@@ -11,10 +11,11 @@ from paper_2304_12152_b200.imagecore import Rng
 pytestmark = pytest.mark.gpu
 
 
-def _run(impl, net, x, dp):
+def _run(impl, net, x, dp, wgrad_parts=2):
     import torch
     from paper_2304_12152_b200 import _lib
     _lib.call("ht_set_train_conv_impl", impl)
+    _lib.call("ht_set_wgrad_parts", wgrad_parts)
     try:
         xd = torch.from_numpy(x.astype(np.float32)).cuda()
         p = net.forward_device(xd)
@@ -24,18 +25,22 @@ def _run(impl, net, x, dp):
         return p.double().cpu().numpy(), grad.cpu().numpy(), dx.double().cpu().numpy()
     finally:
         _lib.call("ht_set_train_conv_impl", 0)
+        _lib.call("ht_set_wgrad_parts", 2)
 
 
 def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("parts", [2, 3])
 @pytest.mark.parametrize("B,H,W", [(3, 40, 52), (1, 96, 150), (1, 7, 300)])
-def test_tensor_core_training_convs_vs_oracle(B, H, W):
+def test_tensor_core_training_convs_vs_oracle(B, H, W, parts):
     """Both the tcgen05 path (impl 0) and the SIMT path (impl 1) against the
     fp64 oracle: p, parameter gradients per tensor and dx within 1e-4
-    relative, and the tensor-core path (split-bf16, short accumulation chains
-    for the large products: ~1e-7 per conv) no less accurate than SIMT."""
+    relative.  With the weight gradient's operands split into three bf16
+    parts (six products) the tensor-core path is no less accurate than SIMT
+    (split-bf16 convs with short accumulation chains: ~1e-7 per conv); the
+    default two parts (three products) stay well inside the 1e-4 bar."""
     from oracle import htoracle as O
     from paper_2304_12152_b200.nn import PolicyNetwork
     net = PolicyNetwork(32, 3)
@@ -50,7 +55,7 @@ def test_tensor_core_training_convs_vs_oracle(B, H, W):
     g_ref = np.concatenate([g.ravel() for g in grads])
     errs = {}
     for impl in (0, 1):
-        p, g, dx = _run(impl, net, x, dp)
+        p, g, dx = _run(impl, net, x, dp, parts)
         assert np.max(np.abs(p - p_ref[:, 0])) < 2e-5
         at = 0
         worst = 0.0
@@ -61,7 +66,10 @@ def test_tensor_core_training_convs_vs_oracle(B, H, W):
             at += n
         errs[impl] = (worst, _rel(g, g_ref), _rel(dx, dx_ref))
         assert worst < 1e-4 and errs[impl][2] < 1e-4, (impl, errs[impl])
-    assert errs[0][1] <= 1.5 * errs[1][1] + 1e-7, errs
+    if parts == 3:
+        assert errs[0][1] <= 1.5 * errs[1][1] + 1e-7, errs
+    else:
+        assert errs[0][0] < 2e-5, errs
 
 
 def test_tensor_core_matches_simt_at_config5_size():
