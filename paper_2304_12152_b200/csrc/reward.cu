@@ -46,6 +46,8 @@ __device__ __forceinline__ double ssim3(double mx, double my, double sxx, double
 }
 
 constexpr int NMAPS = 8;
+constexpr int LE_NQ = 10;   // staged window-centre quantities of the delta kernel
+constexpr int LE_SMEM = (LE_NQ * (RT + 2 * RH) * (RT + 2 * RH) + 2 * RMAXK * RMAXK) * 8;
 // RewardContext's remaining maps (metrics.py:188-204), written on request:
 //   [0] f_h  [1] f_c  [2] luminance  [3] contrast  [4] structure
 //   [5] cssim_map  [6] reward_map
@@ -190,9 +192,13 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
   const int x0 = blockIdx.x * RT, y0 = blockIdx.y * RT;
   const int hk = ks / 2, hw = wsz / 2;
   constexpr int TP = RT + 2 * RH;
-  // b-side maps around the tile: e, mu_h, shc, mu_c, scc, sigma_c, ssim, shh
-  __shared__ double sb[NMAPS][TP][TP];
-  __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
+  // window-centre quantities around the tile, staged once per centre (each
+  // centre serves up to 121 pixels): e, mu_h, shc, shh, mu_c,
+  // mu_c^2 + C1, v_c + C2, sqrt(v_c), sigma_c, SSIM (v_c = max(E[c^2] -
+  // mu_c^2, 0))
+  extern __shared__ double smem_le[];
+  double (*sb)[TP][TP] = reinterpret_cast<double (*)[TP][TP]>(smem_le);
+  double *sk = smem_le + LE_NQ * TP * TP, *sw = sk + RMAXK * RMAXK;
   const size_t n = (size_t)H * W;
   const double *mb = maps + (size_t)b * NMAPS * n;
   for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
@@ -202,8 +208,18 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
     const int gy = y0 + yy - RH, gx = x0 + xx - RH;
     const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
     const size_t idx = in ? (size_t)gy * W + gx : 0;
-#pragma unroll
-    for (int q = 0; q < NMAPS; ++q) sb[q][yy][xx] = in ? mb[q * n + idx] : 0.0;
+    const double muc = in ? mb[3 * n + idx] : 0.0, scc = in ? mb[4 * n + idx] : 0.0;
+    const double vc = fmax(scc - muc * muc, 0.0);
+    sb[0][yy][xx] = in ? mb[0 * n + idx] : 0.0;   // e
+    sb[1][yy][xx] = in ? mb[1 * n + idx] : 0.0;   // mu_h
+    sb[2][yy][xx] = in ? mb[2 * n + idx] : 0.0;   // shc
+    sb[3][yy][xx] = in ? mb[7 * n + idx] : 0.0;   // shh
+    sb[4][yy][xx] = muc;
+    sb[5][yy][xx] = muc * muc + c1;
+    sb[6][yy][xx] = vc + c2;
+    sb[7][yy][xx] = sqrt(vc);
+    sb[8][yy][xx] = in ? mb[5 * n + idx] : 0.0;   // sigma_c
+    sb[9][yy][xx] = in ? mb[6 * n + idx] : 0.0;   // SSIM before
   }
   __syncthreads();
   const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
@@ -244,7 +260,7 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
   // exactly (as in the reference's numpy evaluation; recomputing s1 here
   // could differ from the stored s0 in the last bit)
   if (w_s != 0.0 && d != 0.0) {
-    const double dh = 2.0 * ma * d + d * d;
+    const double dh = 2.0 * ma * d + d * d, dc = d * ca, c3 = c2 / 2.0;
     for (int dy = -hw; dy <= hw; ++dy) {
       const int by = gy - dy;
       if (by < 0 || by >= H) continue;
@@ -253,11 +269,16 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
         if (bx < 0 || bx >= W) continue;
         const double wd = sw[(hw + dy) * wsz + (hw + dx)];
         const int sy = ty + RH - dy, sx = tx + RH - dx;
-        const double muh = sb[1][sy][sx], shc = sb[2][sy][sx], muc = sb[3][sy][sx];
-        const double scc = sb[4][sy][sx], sig = sb[5][sy][sx], s0 = sb[6][sy][sx];
-        const double shh = sb[7][sy][sx];
-        const double s1 = ssim3(muh + wd * d, muc, shh + wd * dh, scc, shc + wd * d * ca, c1, c2);
-        dcs += sig * (s1 - s0);
+        // SSIM_b after the edit (metrics.py:95-107 with the window sums moved
+        // by wd * (d, 2 h d + d^2, d c)), its three factors over one division
+        const double mh = sb[1][sy][sx] + wd * d;
+        const double muc = sb[4][sy][sx], syb = sb[7][sy][sx];
+        const double vx = fmax(sb[3][sy][sx] + wd * dh - mh * mh, 0.0);
+        const double sxv = sqrt(vx);
+        const double cov = sb[2][sy][sx] + wd * dc - mh * muc;
+        const double num = (2.0 * mh * muc + c1) * (2.0 * sxv * syb + c2) * (cov + c3);
+        const double den = (mh * mh + sb[5][sy][sx]) * (vx + sb[6][sy][sx]) * (sxv * syb + c3);
+        dcs += sb[8][sy][sx] * (num / den - sb[9][sy][sx]);
       }
     }
   }
@@ -331,7 +352,8 @@ int ht_reward_signal(const float *p, const double *u, const float *other, const 
   ht::count_launch();
   HT_CHECK_LAUNCH();
   if (signal_out) {
-    ht::reward_le_kernel<float, float><<<grid, 256, 0, st>>>(m_out, p, other, c, H, W, k, ks, w, wsz, c1, c2,
+    if (int rc = ht::ensure_smem_attr((const void *)ht::reward_le_kernel<float, float>, ht::LE_SMEM)) return rc;
+    ht::reward_le_kernel<float, float><<<grid, 256, ht::LE_SMEM, st>>>(m_out, p, other, c, H, W, k, ks, w, wsz, c1, c2,
                                                              w_s, scale, levels - 1, estimator, maps, signal_out);
     ht::count_launch();
     HT_CHECK_LAUNCH();
@@ -396,7 +418,8 @@ int ht_reward_delta_f64(const double *h, const double *other, const double *c, i
   dim3 grid((W + ht::RT - 1) / ht::RT, (H + ht::RT - 1) / ht::RT, B);
   ht::reward_maps_kernel<double><<<grid, 256, 0, st>>>(h, nullptr, c, H, W, k, ks, w, wsz, c1, c2, gain, w_s, 1,
                                                        m, maps, sums, nullptr);
-  ht::reward_le_kernel<double, double><<<grid, 256, 0, st>>>(m, h, other, c, H, W, k, ks, w, wsz, c1, c2, w_s,
+  if (int rc = ht::ensure_smem_attr((const void *)ht::reward_le_kernel<double, double>, ht::LE_SMEM)) return rc;
+  ht::reward_le_kernel<double, double><<<grid, 256, ht::LE_SMEM, st>>>(m, h, other, c, H, W, k, ks, w, wsz, c1, c2, w_s,
                                                              1.0, 1, 2, maps, delta_out);
   ht::count_launch(2);
   HT_CHECK_LAUNCH();
