@@ -597,6 +597,23 @@ def run_ours(args, rank, world, local):
                       "halftone, batches streamed two deep), per rank",
                "bytes_note": "per rank; summed over ranks the copies are the whole batch"}
 
+    # ---- the reference-compatible drop-in call: rl.halftone(net, c, z) with
+    #      numpy float32 (B, H, W) in and float64 (h, p) arrays out, as
+    #      rl.infer_halftone returns them (rl.py:306-311), per rank's shard
+    dropin = None
+    if not args.no_e2e:
+        rl.halftone(net, c_np, z_np)                 # warm (allocations)
+        D.barrier()
+        t0 = time.perf_counter()
+        hd, pd = rl.halftone(net, c_np, z_np)
+        el = D.max(time.perf_counter() - t0)[0]
+        assert np.array_equal(hd.astype(np.uint8), h.cpu().numpy())
+        dropin = {"value": round(B2 * S2 * S2 / el / 1e6, 2), "unit": "Mpixel/s",
+                  "api": "rl.halftone(net, contone, noise): numpy float32 (B,H,W) in, float64 (h, p) out "
+                         "(the reference's return types), one call, wall clock",
+                  "h2d_bytes_per_step": 2 * B * S2 * S2 * 4, "d2h_bytes_per_step": B * S2 * S2 * 5}
+        del hd, pd
+
     # ---- weak scaling (secondary): every rank halftones its own 64 images
     weak = None
     if world > 1:
@@ -660,6 +677,8 @@ def run_ours(args, rank, world, local):
                "clocks": clk.summary()}
         if weak is not None:
             out["weak_scaling"] = weak
+        if dropin is not None:
+            out["e2e_dropin"] = dropin
         if configs:
             out["configs"] = configs
         if functional:

@@ -63,6 +63,26 @@ def test_config2_full_batch_windows():
     assert np.array_equal(p1, p[37]) and np.array_equal(h1, h[37])
 
 
+@pytest.mark.parametrize("i", [0, 63])
+def test_config2_whole_image_vs_oracle(i):
+    """Whole config-2 images (image 0 has a step edge, image 63 does not)
+    from a batched call against the oracle's float64 forward of the whole
+    512^2 image: every pixel by the 1e-3 / band rule (~12 s of oracle)."""
+    from paper_2304_12152_b200 import rl
+    net = _net()
+    c = synth.config_batch(64, 512, 512, seed=2, blobs=8, rects=2, step_frac=0.1).astype(np.float32)
+    z = np.stack([Rng(100 + k).gaussians_f32(512 * 512).reshape(512, 512) for k in (i, 5)])
+    h, p = rl.halftone(net, np.stack((c[i], c[5])), z)
+    params = [q.value for q in net.params()]
+    x = np.stack((c[i], z[0])).astype(np.float64)[None]
+    p_ref = O.policy_forward(params, x)[0, 0]
+    err = np.abs(p[0] - p_ref)
+    assert err.max() <= P_TOL, f"max|dp| {err.max():.2e}"
+    band = np.abs(p_ref - 0.5) < 1e-3
+    assert np.array_equal(h[0][~band], (p_ref >= 0.5)[~band].astype(h.dtype))
+    print(f"image {i}: max|dp| = {err.max():.2e}, mean {err.mean():.2e}, band {band.mean():.4f}")
+
+
 def test_config3_gray_sweep_spectra():
     """256 flat grays g = k/255 at 256^2: halftones (window rule on three
     levels) and the per-level RAPSD / anisotropy of those same halftones."""
