@@ -139,6 +139,25 @@ class TestReward:
         le = O.le_signal(maps, g["m"])
         assert np.max(np.abs(le - g[f"{model}_le"])) < 1e-15
 
+    @pytest.mark.parametrize("model", ["nasanen", "gaussian"])
+    @pytest.mark.parametrize("tag", ["h2", "h4"])
+    def test_context_maps_float64(self, model, tag):
+        """The float64 RewardContext / delta_map fixture (context.npz: inputs
+        that are not float32-representable, binary and 4-level h) against the
+        oracle's restatement."""
+        g = golden("context.npz")
+        key = f"{model}_{tag}"
+        maps = O.RewardMaps(g[tag], g["c"], O.hvs_kernel(model), O.gaussian_kernel(11, 1.5))
+        for ours, ref in (("f_c", "f_c"), ("mu_c", "mu_c"), ("scc", "scc"), ("sigma_c", "sigma_c"),
+                          ("e", "e"), ("mu_h", "mu_h"), ("shh", "shh"), ("shc", "shc"),
+                          ("ssim", "ssim"), ("cssim", "cssim_map"), ("reward_map", "reward_map")):
+            assert np.max(np.abs(getattr(maps, ours) - g[f"{key}_{ref}"])) < 1e-13, ours
+        mse, _, rew = g[f"{key}_scalars"]
+        assert abs(maps.mse - mse) < 1e-14 and abs(maps.reward - rew) < 1e-14
+        other = 1.0 - g["h2"] if tag == "h2" else g["other4"]
+        d = maps.delta_map(other)
+        assert np.max(np.abs(d - g[f"{key}_delta"])) < 1e-15
+
     def test_sampling_draw_order(self):
         g = golden("reward.npz")
         u = O.Rng(10).uniforms(64 * 64).reshape(64, 64)
