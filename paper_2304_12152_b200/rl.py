@@ -58,7 +58,15 @@ def halftone(net, contone, noise, impl=None):
     p = torch.empty(cd.shape, dtype=torch.float32, device=dev)
     h = torch.empty(cd.shape, dtype=torch.uint8, device=dev)
     net.halftone_device(cd, zd, p_out=p, h_out=h, impl=impl, check=True)
-    hp, pp = h.cpu().numpy().astype(np.float64), p.cpu().numpy().astype(np.float64)
+    # float64 results (the reference's types) widened on the device and read
+    # back into page-locked host arrays (torch's host allocator caches the
+    # blocks; each call returns fresh arrays)
+    hp = torch.empty(h.shape, dtype=torch.float64, pin_memory=True)
+    pp = torch.empty(p.shape, dtype=torch.float64, pin_memory=True)
+    hp.copy_(h.double(), non_blocking=True)
+    pp.copy_(p.double(), non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    hp, pp = hp.numpy(), pp.numpy()
     return (hp[0], pp[0]) if single else (hp, pp)
 
 
