@@ -43,6 +43,19 @@ def _torch():
     return torch
 
 
+_libc = None
+
+
+def _memcmp(a, b, n):
+    global _libc
+    if _libc is None:
+        import ctypes
+        _libc = ctypes.CDLL(None)
+        _libc.memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+        _libc.memcmp.restype = ctypes.c_int
+    return _libc.memcmp(a, b, n)
+
+
 def _dev64(a):
     """numpy -> float64 CUDA tensor (CUDA tensors pass through as float64)."""
     torch = _torch()
@@ -145,6 +158,15 @@ class PolicyNetwork:
         self.res = [ResidualBlock(channels) for _ in range(blocks)]
         self.conv_out = Conv2d(channels, 1)
         self._params = self.params()
+        # the host .value arrays are views into one contiguous buffer, so the
+        # per-use "did the host values change?" check is one memory compare
+        # (a caller that rebinds a .value array gets the per-tensor check)
+        self._host = np.zeros(sum(p.value.size for p in self._params))
+        at = 0
+        for p in self._params:
+            n = p.value.size
+            p.value = self._host[at:at + n].reshape(p.value.shape)
+            at += n
         self._dev = None            # torch.device
         self._flat = None           # float64 device params
         self._packed = None         # uint8 device packed weights
@@ -174,7 +196,13 @@ class PolicyNetwork:
         for p in self._params:
             p.grad[...] = 0.0
 
+    def _host_views_intact(self):
+        base = self._host
+        return all(p.value.base is base for p in self._params)
+
     def flat_values(self):
+        if self._host_views_intact():
+            return self._host.copy()
         return np.concatenate([p.value.ravel() for p in self._params])
 
     def set_flat_values(self, flat):
@@ -202,10 +230,12 @@ class PolicyNetwork:
 
     def _host_matches_upload(self):
         """Host .value arrays still equal the last uploaded / pulled values
-        (checked per tensor against views of the snapshot: no concatenation,
-        stops at the first difference)."""
-        at = 0
+        (one compare of the contiguous host buffer; per tensor, stopping at
+        the first difference, if a caller rebound a .value array)."""
         up = self._uploaded
+        if self._host_views_intact() and up.size == self._host.size:
+            return _memcmp(self._host.ctypes.data, up.ctypes.data, self._host.nbytes) == 0
+        at = 0
         for p in self._params:
             n = p.value.size
             if not np.array_equal(p.value.ravel(), up[at:at + n]):

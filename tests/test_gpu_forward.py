@@ -335,3 +335,27 @@ def test_config1_beyond_random_init(case):
     err, band = _check(p, h, p_ref, P_TOL)
     print(f"{case}: max|dp| = {err:.2e}, band fraction {band:.4f}, "
           f"p range [{p_ref.min():.3f}, {p_ref.max():.3f}]")
+
+
+def test_host_parameter_edits_reach_the_device():
+    """Parameter.value arrays are views of one host buffer (one memory
+    compare per use); in-place edits, edits through other views and a
+    rebound .value array all reach the kernels."""
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05, nb=2)
+    c = synth.contone(20, 24, seed=4)
+    z = gaussian_noise_map_f32(Rng(4), 24, 20)
+    _, p0 = rl.halftone(net, c, z)
+    net.conv_out.bias.value[0] += 0.5                      # in place
+    _, p1 = rl.halftone(net, c, z)
+    assert np.all(p1 > p0)
+    net.conv_out.bias.value.reshape(-1)[0] -= 0.5          # through another view
+    _, p2 = rl.halftone(net, c, z)
+    assert np.array_equal(p2, p0)
+    net.conv_out.bias.value = np.array([1.0])              # rebound
+    _, p3 = rl.halftone(net, c, z)
+    assert np.all(p3 > p0)
+    net.conv_out.bias.value = np.array([0.0])
+    _, p4 = rl.halftone(net, c, z)
+    assert np.array_equal(p4, p0)
