@@ -359,3 +359,37 @@ def test_host_parameter_edits_reach_the_device():
     net.conv_out.bias.value = np.array([0.0])
     _, p4 = rl.halftone(net, c, z)
     assert np.array_equal(p4, p0)
+
+
+def test_fp16_overflow_redo_covers_every_output():
+    """The float64 redo (activations beyond fp16's range) fills p, h, the
+    PBM payload and multitone levels like the fused kernel would, on a
+    row window and on a side stream."""
+    import torch
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.1)
+    H, W = 40, 50
+    c = torch.from_numpy(np.stack([synth.contone(H, W, seed=s) for s in (1, 2)])).cuda()
+    z = torch.from_numpy(np.stack([gaussian_noise_map_f32(Rng(s), W, H) for s in (1, 2)])).cuda()
+    params = [q.value.copy() for q in net.params()]
+    p_ref = np.stack([O.halftone(params, c[i].double().cpu().numpy()[5:], z[i].double().cpu().numpy()[5:])[1]
+                      for i in range(2)])
+    rows = (H, 5, 7, H - 12)            # input rows 5.., output rows 7..7+H-12 (window-relative 2..)
+    ci, zi = c[:, 5:].contiguous(), z[:, 5:].contiguous()
+    s = torch.cuda.Stream()
+    p = torch.empty((2, H - 12, W), device="cuda")
+    h = torch.empty((2, H - 12, W), dtype=torch.uint8, device="cuda")
+    pbm = torch.empty((2, H - 12, (W + 7) // 8), dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(s):
+        net.halftone_device(ci, zi, p_out=p, h_out=h, pbm_out=pbm, rows=rows, check=True, stream=s)
+    s.synchronize()
+    want = p_ref[:, 2:2 + H - 12]
+    assert np.max(np.abs(p.cpu().numpy() - want)) < 1e-6
+    hh = h.cpu().numpy()
+    assert np.array_equal(pbm.cpu().numpy(), np.packbits((1 - hh).astype(np.uint8), axis=2))
+    q = torch.empty_like(h)
+    net.halftone_device(ci, zi, h_out=q, rows=rows, check=True, levels=4)
+    levels = np.rint(O.quantize_multitone(want, 4) * 3).astype(np.uint8)   # multitone.py:61-67
+    assert np.array_equal(q.cpu().numpy(), levels)
