@@ -604,17 +604,21 @@ def run_ours(args, rank, world, local):
     #      rl.infer_halftone returns them (rl.py:306-311), per rank's shard
     dropin = None
     if not args.no_e2e:
-        rl.halftone(net, c_np, z_np)                 # warm (allocations)
+        hd, pd = rl.halftone(net, c_np, z_np)        # warm (allocations)
+        assert np.array_equal(hd.astype(np.uint8), h.cpu().numpy())
+        del hd, pd
+        reps = 3
         D.barrier()
         t0 = time.perf_counter()
-        hd, pd = rl.halftone(net, c_np, z_np)
-        el = D.max(time.perf_counter() - t0)[0]
-        assert np.array_equal(hd.astype(np.uint8), h.cpu().numpy())
+        for _ in range(reps):
+            hd, pd = rl.halftone(net, c_np, z_np)
+            del hd, pd
+        el = D.max((time.perf_counter() - t0) / reps)[0]
         dropin = {"value": round(B2 * S2 * S2 / el / 1e6, 2), "unit": "Mpixel/s",
                   "api": "rl.halftone(net, contone, noise): numpy float32 (B,H,W) in, float64 (h, p) out "
-                         "(the reference's return types), one call, wall clock",
-                  "h2d_bytes_per_step": 2 * B * S2 * S2 * 4, "d2h_bytes_per_step": B * S2 * S2 * 5}
-        del hd, pd
+                         "(the reference's return types), wall clock, mean of %d calls; host batches "
+                         "flow in 8 chunks over two streams" % reps,
+                  "h2d_bytes_per_step": 2 * B * S2 * S2 * 4, "d2h_bytes_per_step": B * S2 * S2 * 16}
 
     # ---- weak scaling (secondary): every rank halftones its own 64 images
     weak = None

@@ -37,9 +37,19 @@ def _torch():
 def halftone(net, contone, noise, impl=None):
     """Noise-explicit factoring of rl.infer_halftone (rl.py:309-311):
     returns (h, p) float64 arrays; h = (p >= 0.5) with ties -> 1 (white).
-    contone/noise: (H, W) or batched (B, H, W)."""
-    torch = _torch()
+    contone/noise: (H, W) or batched (B, H, W).  Host batches of >= 4
+    images are pipelined in chunks (_halftone_host_batch)."""
     _lib.require_cuda()
+    net.device
+    if _host_batch(contone) and _host_batch(noise) and np.shape(contone) == np.shape(noise) \
+            and len(np.shape(contone)) == 3 and np.shape(contone)[0] >= _PIPE_MIN_BATCH \
+            and math.prod(np.shape(contone)) > 0:
+        return _halftone_host_batch(net, contone, noise, impl)
+    return _halftone_oneshot(net, contone, noise, impl)
+
+
+def _halftone_oneshot(net, contone, noise, impl):
+    torch = _torch()
     dev = net.device
 
     def as_dev(a):        # numpy / host -> device float32 (CUDA tensors pass through)
@@ -68,6 +78,107 @@ def halftone(net, contone, noise, impl=None):
     torch.cuda.current_stream(dev).synchronize()
     hp, pp = hp.numpy(), pp.numpy()
     return (hp[0], pp[0]) if single else (hp, pp)
+
+
+_PIPE_MIN_BATCH = 4      # host batches of at least this many images are pipelined
+_PIPE_CHUNKS = 8
+_pipe_cache = {}
+
+
+def _host_batch(a):
+    if isinstance(a, np.ndarray):
+        return a.dtype.kind in "fiub"
+    torch = _torch()
+    return isinstance(a, torch.Tensor) and a.device.type == "cpu"
+
+
+def _halftone_host_batch(net, contone, noise, impl):
+    """halftone() for a host batch: the images flow in chunks through
+    host staging (float32, page-locked) -> H2D -> fused K1 -> float64 widening
+    -> D2H into the page-locked result arrays, on two alternating streams, so
+    one chunk's copies and host-side conversion overlap another chunk's
+    kernel.  Same results as the one-shot path (K1 is bitwise batch
+    invariant); a chunk whose fp16 operands overflowed is redone in float64
+    like halftone_device(check=True)."""
+    torch = _torch()
+    dev = net.device
+    B, H, W = (int(x) for x in np.shape(contone))
+    m = -(-B // _PIPE_CHUNKS)
+    bounds = list(range(0, B, m)) + [B]
+    groups = list(zip(bounds[:-1], bounds[1:]))
+    key = (str(dev), m, H, W)
+    res = _pipe_cache.get(key)
+    if res is None:
+        _pipe_cache.clear()              # one shape's buffers at a time
+        res = {
+            "streams": [torch.cuda.Stream(dev, priority=-1) for _ in range(2)],
+            "stage": [torch.empty((2, m, H, W), dtype=torch.float32, pin_memory=True) for _ in range(2)],
+            "inp": [torch.empty((2, m, H, W), dtype=torch.float32, device=dev) for _ in range(2)],
+            "p": [torch.empty((m, H, W), dtype=torch.float32, device=dev) for _ in range(2)],
+            "h": [torch.empty((m, H, W), dtype=torch.uint8, device=dev) for _ in range(2)],
+            "p64": [torch.empty((m, H, W), dtype=torch.float64, device=dev) for _ in range(2)],
+            "h64": [torch.empty((m, H, W), dtype=torch.float64, device=dev) for _ in range(2)],
+            "ws": [None, None],
+            "done": [None, None],
+        }
+        _pipe_cache[key] = res
+    hp = torch.empty((B, H, W), dtype=torch.float64, pin_memory=True)
+    pp = torch.empty((B, H, W), dtype=torch.float64, pin_memory=True)
+
+    def host(a, lo, hi):
+        if isinstance(a, np.ndarray):
+            a = a[lo:hi]
+            if any(s < 0 for s in a.strides) or a.dtype.kind != "f":
+                a = a.astype(a.dtype if a.dtype.kind == "f" else np.float64, order="C", copy=True)
+            return torch.from_numpy(a)
+        return a[lo:hi]
+
+    cur = torch.cuda.current_stream(dev)
+    owner = [None, None]                 # chunk index last run on each slot
+    redo = []
+
+    def retire(s):
+        """Wait for slot s's chunk and check its non-finite flag."""
+        if res["done"][s] is None:
+            return
+        res["done"][s].synchronize()
+        k = owner[s]
+        try:
+            _lib.call("ht_halftone_check", _lib.ptr(res["ws"][s]), _lib.stream_ptr(res["streams"][s]))
+        except FloatingPointError:
+            redo.append(groups[k])
+        res["done"][s] = None
+
+    for k, (a, b) in enumerate(groups):
+        s, n = k % 2, b - a
+        retire(s)                        # staging / device buffers of chunk k-2 are free
+        st = res["stage"][s]
+        st[0, :n].copy_(host(contone, a, b))
+        st[1, :n].copy_(host(noise, a, b))
+        S = res["streams"][s]
+        S.wait_stream(cur)
+        with torch.cuda.stream(S):
+            inp = res["inp"][s]
+            inp[:, :n].copy_(st[:, :n], non_blocking=True)
+            res["ws"][s] = net.halftone_device(inp[0, :n], inp[1, :n], p_out=res["p"][s][:n],
+                                               h_out=res["h"][s][:n], impl=impl, workspace=res["ws"][s],
+                                               stream=S)
+            res["p64"][s][:n].copy_(res["p"][s][:n])
+            res["h64"][s][:n].copy_(res["h"][s][:n])
+            pp[a:b].copy_(res["p64"][s][:n], non_blocking=True)
+            hp[a:b].copy_(res["h64"][s][:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(S)
+        res["done"][s], owner[s] = ev, k
+    for s in range(2):
+        retire(s)
+    for s in range(2):
+        cur.wait_stream(res["streams"][s])
+    hp, pp = hp.numpy(), pp.numpy()
+    for a, b in redo:                    # rare: fp16 overflow -> float64 redo
+        h1, p1 = _halftone_oneshot(net, host(contone, a, b), host(noise, a, b), impl)
+        hp[a:b], pp[a:b] = h1, p1
+    return hp, pp
 
 
 def infer_halftone(net, c, rng, impl=None):

@@ -86,6 +86,34 @@ def test_batch_equals_single_bitwise():
         assert np.array_equal(pi, pb[i]) and np.array_equal(hi, hb[i])
 
 
+def test_host_batch_pipeline_equals_oneshot():
+    """rl.halftone on a host batch of >= 4 images runs chunked through two
+    streams (rl._halftone_host_batch); it equals the one-shot path bitwise
+    for float64 / float32 numpy, reversed-stride views and CPU tensors, with
+    a ragged last chunk, and a chunk that overflows fp16 is redone in float64
+    like the one-shot path."""
+    import torch
+    from paper_2304_12152_b200 import rl, synth
+    from paper_2304_12152_b200.imagecore import Rng, gaussian_noise_map_f32
+    net = _net(0.05)
+    B = 11                                        # chunks of 2, the last of 1
+    cs = synth.config_batch(B, 40, 52, seed=5, step_frac=0.3).astype(np.float64)
+    zs = np.stack([gaussian_noise_map_f32(Rng(30 + i), 52, 40) for i in range(B)])
+    h1, p1 = rl._halftone_oneshot(net, cs, zs, None)
+    for c, z, rev in ((cs, zs, False), (cs.astype(np.float32), zs, False), (cs[::-1], zs[::-1], True),
+                      (torch.from_numpy(cs), torch.from_numpy(zs), False)):
+        h, p = rl.halftone(net, c, z)
+        assert h.dtype == np.float64 and p.dtype == np.float64 and h.shape == (B, 40, 52)
+        if rev:
+            h, p = h[::-1], p[::-1]
+        assert np.array_equal(p, p1) and np.array_equal(h, h1)
+    big = _net(0.1)                               # activations leave fp16's range
+    cs4, zs4 = cs[:5, :24, :20], zs[:5, :24, :20]
+    hb, pb = rl.halftone(big, cs4, zs4)
+    ho, po = rl._halftone_oneshot(big, cs4, zs4, None)
+    assert np.array_equal(pb, po) and np.array_equal(hb, ho)
+
+
 def test_row_window_sharding_bitwise():
     """Config-4 style row strips with the 34-row receptive-field halo."""
     import torch
