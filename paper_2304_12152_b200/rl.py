@@ -11,6 +11,7 @@ GLOBAL 1/batch_size and w_a/ba, rl.py:253, 272).
 """
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,7 +45,8 @@ def halftone(net, contone, noise, impl=None):
     if _host_batch(contone) and _host_batch(noise) and np.shape(contone) == np.shape(noise) \
             and len(np.shape(contone)) == 3 and np.shape(contone)[0] >= _PIPE_MIN_BATCH \
             and math.prod(np.shape(contone)) > 0:
-        return _halftone_host_batch(net, contone, noise, impl)
+        with _pipe_lock:
+            return _halftone_host_batch(net, contone, noise, impl)
     return _halftone_oneshot(net, contone, noise, impl)
 
 
@@ -83,6 +85,7 @@ def _halftone_oneshot(net, contone, noise, impl):
 _PIPE_MIN_BATCH = 4      # host batches of at least this many images are pipelined
 _PIPE_CHUNKS = 8
 _pipe_cache = {}
+_pipe_lock = threading.Lock()      # the cached staging buffers serve one call at a time
 
 
 def _host_batch(a):
