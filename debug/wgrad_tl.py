@@ -27,6 +27,7 @@ wait_full = m[:n, 3] - m[:n, 1]
 print(" issue-to-issue cycles: mean %.0f median %.0f" % (np.diff(iss).mean(), np.median(np.diff(iss))))
 print(" wait (d_empty) mean %.0f, wait(full)+issue mean %.0f" % ((m[:n, 1] - m[:n, 0]).mean(), wait_full.mean()))
 c = a[0]; k = int((c[:, 3] > 0).sum())
+print(f"converters (warp 0): wait raw {np.mean(c[:k,2]-c[:k,0]):.0f}, then op_free {np.mean(c[:k,1]-c[:k,2]):.0f}")
 print(f"converters (warp 0): tiles {k}  wait(raw+op) {np.mean(c[:k,1]-c[:k,0]):.0f}  convert {np.mean(c[:k,3]-c[:k,1]):.0f}  "
       f"period {np.mean(np.diff(c[:k,0])):.0f}")
 fl = a[9]; k = int((fl[:, 3] > 0).sum())

@@ -66,7 +66,6 @@ constexpr int DBOX = 44;
 constexpr int RAW_X = XR * C * WT * 4;          // 16 KB, 128-B swizzled rows (y, c)
 constexpr int RAW_D = TY * C * DBOX * 4;        // 11 KB
 constexpr int RAW_SLOT = (RAW_X + RAW_D + 1023) / 1024 * 1024;
-constexpr int NB = 2;                 // operand buffers
 constexpr uint32_t IDESC =
     (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 // TMEM: chain accumulator D (192 columns), the x operand A (NB buffers x NP
@@ -78,6 +77,12 @@ struct Lay {
   static constexpr int NPROD = NP == 2 ? 3 : 6;
   static constexpr int F = NP == 2 ? 16 : 8;        // tiles per accumulation chain (96 MMAs)
   static constexpr int NR = 4;                       // raw ring slots
+  // operand buffers: converters fill tile t+NB-1 while the MMAs of tile t run
+  // (three for two parts: the converters then never wait on the MMAs' commit
+  // round trip; the x operands of NB buffers x NP parts fit TMEM columns
+  // 192..287 either way)
+  static constexpr int NB = NP == 2 ? 3 : 2;
+  static_assert(A_COL + NB * NP * 16 <= D2_COL, "TMEM operand buffers overlap D2");
   static constexpr int D_ROW = 3 * ROWB;   // three kx-shifted copies of a dout row
   static constexpr int D_PART = TY * D_ROW;
   static constexpr int BUF = (NP * D_PART + 1023) / 1024 * 1024;   // dout operand (B) only
@@ -170,8 +175,8 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
   uint8_t *smem = smem_raw + (sbase - sraw);
   const uint32_t raw_full0 = sbase + L::BAR_OFF, raw_empty0 = raw_full0 + 8 * L::NR;
-  const uint32_t op_full0 = raw_empty0 + 8 * L::NR, op_free0 = op_full0 + 8 * NB;
-  const uint32_t d_full = op_free0 + 8 * NB, d_empty = d_full + 8;
+  const uint32_t op_full0 = raw_empty0 + 8 * L::NR, op_free0 = op_full0 + 8 * L::NB;
+  const uint32_t d_full = op_free0 + 8 * L::NB, d_empty = d_full + 8;
   float *db_s = reinterpret_cast<float *>(smem + L::DB_OFF);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::TMEMP_OFF);
   if (tid == 0) {
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
       mbar_init(raw_full0 + 8 * i, 1);
       mbar_init(raw_empty0 + 8 * i, NCONV / 32);
     }
-    for (int i = 0; i < NB; ++i) {
+    for (int i = 0; i < L::NB; ++i) {
       mbar_init(op_full0 + 8 * i, NCONV / 32);
       mbar_init(op_free0 + 8 * i, 1);
     }
@@ -213,12 +218,15 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
     const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL + xh * 8;
     float dbacc = 0.f;
     for (int i_t = 0; i_t < n_tiles; ++i_t) {
-      const int slot = i_t % L::NR, q = i_t % NB;
+      const int slot = i_t % L::NR, q = i_t % L::NB;
       const long long tl0 = clock64();
+      long long tlr = 0;
       if (lane == 0) {
         mbar_wait(raw_full0 + 8 * slot, (i_t / L::NR) & 1);
-        if (i_t >= NB) mbar_wait(op_free0 + 8 * q, ((i_t / NB) - 1) & 1);
+        tlr = clock64();
+        if (i_t >= L::NB) mbar_wait(op_free0 + 8 * q, ((i_t / L::NB) - 1) & 1);
       }
+      (void)tlr;
       __syncwarp();
       tc_fence_after();
       const long long tl1 = clock64();
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
         mbar_arrive(raw_empty0 + 8 * slot);
         mbar_arrive(op_full0 + 8 * q);
       }
-      if (warp == 0) WTL(0, i_t, tl0, tl1, 0);
+      if (warp == 0) WTL(0, i_t, tl0, tl1, tlr);
     }
     if (!xw && u < D_UNITS) atomicAdd(&db_s[c], dbacc);
   } else if (warp == L::TMA_WARP) {
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
     // ---- MMA warp: tiles in order; chains of F tiles into D (the first MMA
     //      of a chain overwrites it), each handed to the flushers
     for (int i_t = 0; i_t < n_tiles; ++i_t) {
-      const int q = i_t % NB;
+      const int q = i_t % L::NB;
       const int f = i_t / L::F;
       const bool chain_start = i_t % L::F == 0;
       const bool chain_end = i_t % L::F == L::F - 1 || i_t == n_tiles - 1;
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
       if (lane == 0) {
         if (chain_start && f >= 1) mbar_wait(d_empty, (f - 1) & 1);
         tm1 = clock64();
-        mbar_wait(op_full0 + 8 * q, (i_t / NB) & 1);
+        mbar_wait(op_full0 + 8 * q, (i_t / L::NB) & 1);
       }
       __syncwarp();
       tc_fence_after();
