@@ -325,7 +325,16 @@ conv3x3_wgrad32_kernel(const float *__restrict__ x, const float *__restrict__ do
 // conv_tc.cu: the 32 -> 32 training conv on tcgen05 (split-bf16, fp32-level)
 int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
               const float *resid, float *out, int relu, cudaStream_t st);
-extern int g_train_conv_impl;   // 0: tensor cores for 32 -> 32 convs (default), 1: SIMT only
+// conv_tc2.cu: the same conv with scaled fp16 pairs and role-split warps
+// (half the MMAs; TMA-staged shapes only)
+bool conv_tc2_eligible(int W);
+int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+                const float *resid, float *out, int relu, cudaStream_t st);
+// 0: tensor cores for 32 -> 32 convs (default: conv_tc2 for launches without
+// a mask / residual input, conv_tc otherwise), 1: SIMT only, 2: tensor cores
+// with conv_tc.cu's split-bf16 kernel everywhere, 3: conv_tc2 wherever the
+// shape allows (A/B and tests)
+extern int g_train_conv_impl;
 // wgrad_tc.cu: their weight gradient on tcgen05 (split-bf16, `parts` bf16 parts)
 int wgrad_tc32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int parts,
                cudaStream_t st);
@@ -336,7 +345,14 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
                     const float *mask, const float *resid, float *out, int relu,
                     cudaStream_t st) {
   if constexpr (CIN == 32 && COUT == 32) {
-    if (g_train_conv_impl == 0) return conv_tc32(x, B, H, W, w, bias, mask, resid, out, relu, st);
+    // conv_tc2 where it measured faster: launches without a mask / residual
+    // input (the forward conv1s; 20 x 256^2: 115 vs 134 us).  With one, its
+    // drainers wait on the input's loads (175 vs 161 us), so conv_tc runs those.
+    if (g_train_conv_impl == 0 && conv_tc2_eligible(W) && !mask && !resid)
+      return conv_tc2_32(x, B, H, W, w, bias, mask, resid, out, relu, st);
+    if (g_train_conv_impl == 3 && conv_tc2_eligible(W) && !(mask && resid))
+      return conv_tc2_32(x, B, H, W, w, bias, mask, resid, out, relu, st);
+    if (g_train_conv_impl != 1) return conv_tc32(x, B, H, W, w, bias, mask, resid, out, relu, st);
   }
   dim3 grid((W + FT_X - 1) / FT_X, (H + FT_Y - 1) / FT_Y, B);
   conv3x3_fwd_kernel<CIN, COUT><<<grid, 128, 0, st>>>(x, H, W, w, bias, mask, resid, out, relu);
@@ -350,7 +366,7 @@ static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, do
                       double *db, cudaStream_t st) {
   if constexpr (CIN == 32 && COUT == 32) {
     // the tensor-core kernel streams rows with TMA (16-B row strides: W % 4 == 0)
-    if (g_train_conv_impl == 0 && W % 4 == 0) return wgrad_tc32(x, dout, B, H, W, dw, db, g_wgrad_parts, st);
+    if (g_train_conv_impl != 1 && W % 4 == 0) return wgrad_tc32(x, dout, B, H, W, dw, db, g_wgrad_parts, st);
     const size_t smem = sizeof(float) * ((size_t)32 * (W32_TY + 2) * (W32_TX + 2) + W32_TY * W32_TX * W32_PAD);
     if (int rc = ensure_smem_attr((const void *)conv3x3_wgrad32_kernel, (int)smem)) return rc;
     const long tiles = (long)B * ((W + W32_TX - 1) / W32_TX) * ((H + W32_TY - 1) / W32_TY);
@@ -572,7 +588,7 @@ int ht_policy_backward(const void *packed, int C, int NB, const float *x, int B,
 int ht_conv3x3_32(const float *x, int B, int H, int W, const float *w, const float *bias,
                   const float *mask, const float *resid, float *out, int relu, int impl, void *stream) {
   HT_REQUIRE(B >= 1 && H >= 1 && W >= 1, "empty input");
-  HT_REQUIRE(impl == 0 || impl == 1, "impl must be 0 (tensor core) or 1 (simt)");
+  HT_REQUIRE(impl >= 0 && impl <= 3, "impl must be 0 (tensor core), 1 (simt), 2 (split bf16) or 3 (fp16 pairs)");
   const int keep = ht::g_train_conv_impl;
   ht::g_train_conv_impl = impl;
   const int rc = ht::conv_fwd<32, 32>(x, B, H, W, w, bias, mask, resid, out, relu, (cudaStream_t)stream);

@@ -1,0 +1,550 @@
+// Training 3x3 convolution 32 -> 32 on tcgen05, version 2: scaled fp16 pairs
+// and role-split warps.  Same contract as conv_tc.cu (the residual blocks'
+// forward convs nn.py:46-60, 91-95 and their input gradients nn.py:62-77,
+// 97-100, run as forward convs with transposed / flipped weights): NCHW fp32
+// in and out, epilogue bias, ReLU mask, residual add, ReLU.
+//
+// Precision: every input row x is scaled by a power of two 2^sx (row max |x|
+// -> [2^13, 2^14)) and split into two fp16 parts x0 + x1 (x1 = the fp16
+// rounding of the remainder: 22 significant bits), the weights likewise with
+// one per-layer scale 2^sw.  A row's products x0 w0 + x0 w1 + x1 w0 (three
+// kind::f16 MMAs per tap and K-half, 18 per row) accumulate in fp32 in the
+// row's own TMEM ring, and the drain multiplies each ring by 2^-(sx + sw)
+// (exact) before summing the three rings of an output row.  Error ~2^-22
+// of the row scale per product -- the SIMT fp32 class; the per-row scale keeps
+// the tiny input gradients of the backward pass (1e-9 and below) in fp16's
+// normal range.  conv_tc.cu's split bf16 needs six products for the same
+// class (bf16 has 8 significant bits).
+//
+// Structure (one CTA per SM, strips of 128 pixel lanes with 126 output lanes,
+// rows streamed top to bottom, MMA(x) for input row x adding into output rows
+// x+1, x, x-1 of TMEM ring x mod 4 through the doubled-ky B window):
+// * issuer warp: TMA of input row x+3 into a 3-slot staging ring, then the 18
+//   MMAs of row x once the splitters have written it and the drainers have
+//   freed ring x mod 4;
+// * 4 splitter warps (thread = pixel lane, 32 channels): staged row -> row
+//   max (warp reduce + 4-warp barrier) -> scaled fp16 pair planes in one of
+//   three A buffers.  They touch no global memory, so the proxy fence that
+//   publishes the planes to the tensor core waits for nothing else;
+// * 8 drainer warps (thread = pixel lane x 16 channels): wait for the MMAs of
+//   an output row's three input rows, unscale and sum the rings, epilogue,
+//   coalesced NCHW stores, and the next row's mask / residual loads.
+// Splitting, MMAs and draining of different rows overlap: the tensor pipe
+// works on MMA(x) while row x+1 is split and row x-2 is drained.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+#include <cuda_fp16.h>
+
+namespace ht {
+namespace tct2 {
+
+using namespace ::ht::tc;
+
+constexpr int C = 32;
+constexpr int M = 128;
+constexpr int S = M - 2;                  // output lanes per strip
+constexpr int NSL = 5;                    // doubled ky sequence [2,1,0,2,1]
+constexpr int NPART = 2;                  // fp16 parts
+constexpr int PLANE = M * 16;             // 8 channels x 128 lanes (fp16)
+constexpr int ROW = 4 * PLANE;            // 32 channels of a row, one part
+constexpr int TILE = 2 * NSL * C * 16;    // B tile (kx, K-half): 160 rows x 2 K-chunks x 16 B
+constexpr int W_BYTES = NPART * 6 * TILE;
+constexpr int NAB = 3;                    // A buffers
+constexpr int A_OFF = W_BYTES;
+constexpr int A_BYTES = NAB * NPART * ROW;
+constexpr int NSTG = 3;                   // staging slots (TMA three rows ahead)
+constexpr int BOXW = M + 4;               // box: 132 px x 32 channels fp32, [ch][px]
+constexpr int BOX = BOXW * C * 4;
+constexpr int STG_SLOT = 2 * BOX;         // a strip row spans at most two images
+constexpr int STG_OFF = A_OFF + A_BYTES;
+constexpr int BAR_OFF = STG_OFF + NSTG * STG_SLOT;
+constexpr int NRING = 4;                  // TMEM rings of 96 columns
+// barriers (8 B each): acc_full[4], ready[4], ring_free[4], stg_full[3], stg_empty[3]
+constexpr int B_ACC = 0, B_RDY = 4, B_FREE = 8, B_STG = 12, B_STE = 15, NBARS = 18;
+constexpr int MISC_OFF = BAR_OFF + NBARS * 8;   // tmem slot, pad, sx[8], red[2][8], wred[24]
+constexpr int SMEM = MISC_OFF + 384;
+constexpr int NSPL = 128, NDRN = 256;
+constexpr int NISS = 2;                         // MMA issuer warps (even / odd rows)
+constexpr int NTHR = NSPL + NDRN + 32 * NISS + 32;   // + issuers + TMA producer warp
+constexpr int HC = C / 2;
+constexpr int SCALE_TOP = 14;             // scaled max |x| in [2^(SCALE_TOP-1), 2^SCALE_TOP)
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+static_assert(STG_OFF % 1024 == 0 && BOX % 128 == 0, "TMA destinations must stay 128-B aligned");
+static_assert(SMEM <= 232448, "shared memory exceeded");
+__constant__ int c_ky2[NSL] = {2, 1, 0, 2, 1};
+
+__device__ __forceinline__ float exp2i(int e) { return __int_as_float((127 + e) << 23); }
+// scale exponent of a block whose max |x| is m (0 / NaN -> 0), clamped to +-60
+__device__ __forceinline__ int scale_exp(float m) {
+  if (!(m > 0.f)) return 0;
+  const int e = ((__float_as_int(m) >> 23) & 0xff) - 127;
+  return max(-60, min(60, SCALE_TOP - 1 - e));
+}
+// v = x0 + x1 with x0 = fp16(v), x1 = fp16(v - x0); pairs packed as half2
+__device__ __forceinline__ void split2h(float a, float b, uint32_t &p0, uint32_t &p1) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+  p0 = *reinterpret_cast<const uint32_t *>(&h);
+  p1 = *reinterpret_cast<const uint32_t *>(&l);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+// three 16-column TMEM loads, one wait
+__device__ __forceinline__ void tmem_ld16x3(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t (&r)[3][16]) {
+#define HT_LD16(T, R)                                                                                          \
+  asm volatile(                                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+      : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]), "=r"(R[7]),       \
+        "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]), "=r"(R[14]), "=r"(R[15])  \
+      : "r"(T))
+  HT_LD16(t0, r[0]);
+  HT_LD16(t1, r[1]);
+  HT_LD16(t2, r[2]);
+#undef HT_LD16
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+#ifdef CT2_TL
+// debug timeline of CTA 0 (lane 0 of the issuer, splitter warp 0, drainer
+// warp 4): [role][row][event] = clock64
+__device__ long long g_ctl2[3][1024][6];
+#define TL2(role, n, k) do { if (blockIdx.x == 0 && lane == 0 && (n) < 1024) g_ctl2[role][n][k] = clock64(); } while (0)
+#else
+#define TL2(role, n, k) do {} while (0)
+#endif
+
+struct Conv2Params {
+  CUtensorMap tm_x;   // x as (W, C, H, B) fp32, box 132 x 32 x 1 x 1
+  const float *w, *bias, *mask, *resid;
+  float *out;
+  int B, H, W, VW, relu;
+  int n_strips;
+  long long chunk;    // strip-rows per CTA (strip-major)
+};
+
+// the strip-major (strip, row) range [q0, q1) of a CTA, walked as segments
+struct Seg {
+  int s, R0, R1, A, Bn;
+};
+__device__ __forceinline__ long long next_seg(long long qq, long long q1, int H, Seg &g) {
+  g.s = (int)(qq / H);
+  const long long end = min(q1, (long long)(g.s + 1) * H);
+  g.R0 = (int)(qq - (long long)g.s * H);
+  g.R1 = (int)(end - (long long)g.s * H);
+  g.A = max(g.R0 - 1, 0);
+  g.Bn = min(g.R1 + 1, H);
+  return end;
+}
+
+__global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant__ Conv2Params P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int k) { return sbase + BAR_OFF + 8u * (uint32_t)k; };
+  auto acc_full = [&](long long g) { return bar(B_ACC + (int)(g & 3)); };
+  auto ready = [&](long long g) { return bar(B_RDY + (int)(g & 3)); };
+  auto ring_free = [&](long long g) { return bar(B_FREE + (int)(g & 3)); };
+  auto stg_full = [&](long long g) { return bar(B_STG + (int)(g % NSTG)); };
+  auto stg_empty = [&](long long g) { return bar(B_STE + (int)(g % NSTG)); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + MISC_OFF);
+  int *sx_s = reinterpret_cast<int *>(smem + MISC_OFF + 8);        // [8] row scale by g & 7
+  int *red = reinterpret_cast<int *>(smem + MISC_OFF + 48);        // [2][8] row-max partials
+  int *wred = reinterpret_cast<int *>(smem + MISC_OFF + 112);      // [24] weight-max partials
+  float *bias_s = reinterpret_cast<float *>(smem + MISC_OFF + 208); // [32] bias
+  if (tid == 0) {
+    for (int k = 0; k < 4; ++k) {
+      mbar_init(bar(B_ACC + k), 1);
+      mbar_init(bar(B_RDY + k), NSPL / 32);
+      mbar_init(bar(B_FREE + k), NDRN / 32);
+    }
+    for (int k = 0; k < NSTG; ++k) {
+      mbar_init(bar(B_STG + k), 1);
+      mbar_init(bar(B_STE + k), NSPL / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // ---- weights: per-layer scale, two fp16 parts in UMMA tiles [part][kx][kh]
+  {
+    float m = 0.f;
+    for (int i = tid; i < C * C * 9; i += NTHR) m = fmaxf(m, fabsf(__ldg(P.w + i)));
+    m = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(m)));
+    if (lane == 0) wred[warp] = __float_as_int(m);
+  }
+  __syncthreads();
+  int sw;
+  {
+    float m = 0.f;
+    for (int k = 0; k < NTHR / 32; ++k) m = fmaxf(m, __int_as_float(wred[k]));
+    sw = scale_exp(m);
+  }
+  const float wsc = exp2i(sw);
+  for (int i = tid; i < 3 * 2 * 2 * NSL * C * 4; i += NTHR) {
+    // one (e pair) of a B row: 2 channels -> 4 B per part
+    const int ep = i & 3, co = (i >> 2) % C, s = (i >> 2) / C % NSL;
+    const int kc = (i >> 2) / C / NSL % 2, kh = (i >> 2) / C / NSL / 2 % 2, kx = (i >> 2) / C / NSL / 4;
+    const int ci = kh * 16 + kc * 8 + 2 * ep, ky = c_ky2[s];
+    const float wa = __ldg(P.w + ((co * C + ci) * 3 + ky) * 3 + kx) * wsc;
+    const float wb = __ldg(P.w + ((co * C + ci + 1) * 3 + ky) * 3 + kx) * wsc;
+    uint32_t p0, p1;
+    split2h(wa, wb, p0, p1);
+    const int off = (kx * 2 + kh) * TILE + kc * (NSL * C * 16) + (s * C + co) * 16 + ep * 4;
+    *reinterpret_cast<uint32_t *>(smem + off) = p0;
+    *reinterpret_cast<uint32_t *>(smem + 6 * TILE + off) = p1;
+  }
+  for (int i = tid; i < A_BYTES / 16; i += NTHR)
+    reinterpret_cast<uint4 *>(smem + A_OFF)[i] = make_uint4(0, 0, 0, 0);
+  if (tid < C) bias_s[tid] = P.bias ? __ldg(P.bias + tid) : 0.f;
+  fence_proxy_async();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const size_t plane = (size_t)P.H * P.W;
+  const long long q0 = (long long)blockIdx.x * P.chunk;
+  const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * P.H);
+  const int WP = P.W + 1;
+
+  if (warp == (NSPL + NDRN) / 32 + NISS) {
+    // ================= producer: input rows by TMA, NSTG rows ahead ========
+    if (lane == 0) {
+      long long tg = 0;
+      for (long long qq = q0; qq < q1;) {
+        Seg sg;
+        qq = next_seg(qq, q1, P.H, sg);
+        const int v0 = sg.s * S - 1, b0 = max(v0, 0) / WP;
+        const int nbox = (b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
+        const int c0a = (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
+        for (int x = sg.A; x < sg.Bn; ++x, ++tg) {
+          // slot tg % NSTG was read by the splitters of row tg - NSTG
+          if (tg >= NSTG) mbar_wait(stg_empty(tg), (uint32_t)((tg / NSTG) - 1) & 1u);
+          const uint32_t fb = stg_full(tg), dst = sbase + STG_OFF + (uint32_t)(tg % NSTG) * STG_SLOT;
+#ifdef KO_TMA
+          mbar_arrive(fb);
+#else
+          mbar_expect_tx(fb, nbox * BOX);
+          tma_load_4d(dst, &P.tm_x, c0a, 0, x, b0, fb);
+          if (nbox == 2) tma_load_4d(dst + BOX, &P.tm_x, c0b, 0, x, b0 + 1, fb);
+#endif
+        }
+      }
+    }
+  } else if (warp >= (NSPL + NDRN) / 32) {
+    // ================= issuers: 18 MMAs per row, rows alternating between two
+    // warps: while one warp's issue blocks on the tensor pipe's queue, the
+    // other waits for its next row's inputs and ring, so the pipe is fed with
+    // no gap between batches
+    const int iss = warp - (NSPL + NDRN) / 32;
+    const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
+    const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)((NSL * C * 16) >> 4) << 16);
+    long long g = 0;
+    for (long long qq = q0; qq < q1;) {
+      Seg sg;
+      qq = next_seg(qq, q1, P.H, sg);
+      int xm3 = sg.A % 3;
+      for (int x = sg.A; x < sg.Bn; ++x, ++g, xm3 = xm3 == 2 ? 0 : xm3 + 1) {
+        if ((int)(g % NISS) != iss) continue;
+        TL2(0, g, 0);
+#ifndef KO_NOWAIT
+        if (lane == 0) mbar_wait(ready(g), (uint32_t)(g >> 2) & 1u);
+#endif
+        __syncwarp();
+        TL2(0, g, 1);
+        TL2(0, g, 2);
+        if (g >= NRING) {
+#ifndef KO_NOWAIT
+          if (lane == 0) mbar_wait(ring_free(g), (uint32_t)((g >> 2) - 1) & 1u);
+#endif
+          __syncwarp();
+        }
+        TL2(0, g, 3);
+        tc_fence_after();
+        if (lane == 0) {
+          const int o = xm3 == 0 ? 1 : (xm3 == 1 ? 0 : 2);   // B window for rows (x+1, x, x-1)
+          const uint32_t d = tmem + (uint32_t)((g & 3) * 3 * C);
+          const uint64_t a0 = adesc0 + ((A_OFF + (uint32_t)(g % NAB) * NPART * ROW) >> 4);
+          const uint64_t b0 = bdesc0 + ((o * C * 16) >> 4);
+          constexpr uint64_t AP = ROW >> 4, BP = (6 * TILE) >> 4, TB = TILE >> 4, KH = (2 * PLANE) >> 4;
+          // corrections x1 w0 and x0 w1 first (the first one overwrites the
+          // ring), the main products x0 w0 last
+          uint32_t acc = 0;
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+              const uint64_t a = a0 + kh * KH + kx - 1, b = b0 + (kx * 2 + kh) * TB;
+              mma_f16(d, a + AP, b, acc);
+              acc = 1;
+              mma_f16(d, a, b + BP, 1);
+            }
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) mma_f16(d, a0 + kh * KH + kx - 1, b0 + (kx * 2 + kh) * TB, 1);
+          tc_commit(acc_full(g));
+        }
+        __syncwarp();
+        TL2(0, g, 4);
+      }
+    }
+  } else if (warp < NSPL / 32) {
+    // ================= splitters: staged row -> scaled fp16 pair planes =====
+    const int l = tid;   // pixel lane, all 32 channels
+    long long g = 0;
+    for (long long qq = q0; qq < q1;) {
+      Seg sg;
+      qq = next_seg(qq, q1, P.H, sg);
+      const int v0 = sg.s * S - 1, v = v0 + l;
+      const int b = v >= 0 ? v / WP : 0, col = v >= 0 ? v % WP : 0;
+      const bool in_img = v >= 0 && v < P.VW && col < P.W;
+      const int b0 = max(v0, 0) / WP;
+      const int kbox = in_img ? b - b0 : -1;
+      const int kcol = v0 - (b0 + max(kbox, 0)) * WP;
+      const int koff = l + (kcol & 3);
+      for (int x = sg.A; x < sg.Bn; ++x, ++g) {
+        if (warp == 0) TL2(1, g, 0);
+        if (lane == 0) mbar_wait(stg_full(g), (uint32_t)(g / NSTG) & 1u);
+        __syncwarp();
+        if (warp == 0) TL2(1, g, 1);
+#ifdef KO_SPLIT
+        if (lane == 0) mbar_arrive(stg_empty(g));
+        if (g >= NAB) { if (lane == 0) mbar_wait(acc_full(g - NAB), (uint32_t)((g - NAB) >> 2) & 1u); __syncwarp(); }
+        if (tid == 0) sx_s[g & 7] = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ready(g));
+        continue;
+#endif
+        float xin[C];
+        const float *src = reinterpret_cast<const float *>(smem + STG_OFF + (uint32_t)(g % NSTG) * STG_SLOT +
+                                                           max(kbox, 0) * BOX) + koff;
+        float m = 0.f;
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          xin[i] = kbox >= 0 ? src[i * BOXW] : 0.f;
+          m = fmaxf(m, fabsf(xin[i]));
+        }
+        m = __int_as_float(__reduce_max_sync(0xffffffffu, __float_as_int(m)));
+        // this warp's reads of the staging slot are done
+        if (lane == 0) {
+          mbar_arrive(stg_empty(g));
+          red[(g & 1) * 4 + warp] = __float_as_int(m);
+        }
+        named_bar(1, NSPL);
+        {
+          const int4 ra = *reinterpret_cast<const int4 *>(red + (g & 1) * 4);
+          m = __int_as_float(max(max(ra.x, ra.y), max(ra.z, ra.w)));
+        }
+        const int sx = scale_exp(m);
+        const float sc = exp2i(sx);
+        if (warp == 0) TL2(1, g, 2);
+        // A buffer g % NAB was last read by MMA(g - NAB)
+        if (g >= NAB) {
+          if (lane == 0) mbar_wait(acc_full(g - NAB), (uint32_t)((g - NAB) >> 2) & 1u);
+          __syncwarp();
+        }
+        if (warp == 0) TL2(1, g, 3);
+        const uint32_t dst = sbase + A_OFF + (uint32_t)(g % NAB) * NPART * ROW + l * 16;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          uint32_t h[4], lo[4];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2)
+            split2h(xin[8 * kc + 2 * k2] * sc, xin[8 * kc + 2 * k2 + 1] * sc, h[k2], lo[k2]);
+          st_shared_v4(dst + kc * PLANE, h[0], h[1], h[2], h[3]);
+          st_shared_v4(dst + ROW + kc * PLANE, lo[0], lo[1], lo[2], lo[3]);
+        }
+        if (tid == 0) sx_s[g & 7] = sx;
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ready(g));
+        if (warp == 0) TL2(1, g, 4);
+      }
+    }
+  } else {
+    // ================= drainers: rings -> output rows =======================
+    const int wd = warp - NSPL / 32;
+    const int wq = warp & 3, half = wd >> 2;
+    const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16);
+    const int l = wq * 32 + lane, c0 = half * HC;
+    // the one epilogue input of a launch (the training path passes a ReLU
+    // mask or a residual, never both: conv_tc2_32 requires that), two row
+    // buffers: row d+1's loads are issued before row d's drain, a whole row
+    // period ahead of their use, with no register copy in between
+    float bv[HC];
+#pragma unroll
+    for (int i = 0; i < HC; ++i) bv[i] = P.bias ? __ldg(P.bias + c0 + i) : 0.f;
+    const float *epi = P.mask ? P.mask : P.resid;
+    const bool is_mask = P.mask != nullptr;
+    float ea[HC], eb[HC];
+    long long gbase = 0;
+    for (long long qq = q0; qq < q1;) {
+      Seg sg;
+      qq = next_seg(qq, q1, P.H, sg);
+      const int v = sg.s * S - 1 + l;
+      const int b = v >= 0 ? v / WP : 0, col = v >= 0 ? v % WP : 0;
+      const bool in_img = v >= 0 && v < P.VW && col < P.W;
+      const bool lane_valid = l >= 1 && l < 1 + S && in_img;
+      const size_t obase = ((size_t)b * C + c0) * plane + col;
+      auto gx = [&](int x) { return gbase + (x - sg.A); };
+      auto release = [&](int x) {   // ring of input row x: every output row it feeds is drained
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ring_free(gx(x)));
+      };
+      auto load_epi = [&](int row, float (&e)[HC]) {
+        if (!epi || !(row < sg.R1 && lane_valid)) return;
+        const float *src = epi + obase + (size_t)row * P.W;
+#pragma unroll
+        for (int i = 0; i < HC; ++i) e[i] = __ldg(src + (size_t)i * plane);
+      };
+      auto drain_row = [&](int d, const float (&e)[HC], float (&e_next)[HC]) {
+        load_epi(d + 1, e_next);
+        // MMAs of input rows d-1, d, d+1 done (two issuer warps: no order
+        // between their commits, so each is waited for)
+        if (warp == 4) TL2(2, gx(d), 0);
+        if (lane == 0) {
+          for (int xr = max(d - 1, sg.A); xr <= min(d + 1, sg.Bn - 1); ++xr) {
+            const long long gt = gx(xr);
+            mbar_wait(acc_full(gt), (uint32_t)(gt >> 2) & 1u);
+          }
+        }
+        __syncwarp();
+        if (warp == 4) TL2(2, gx(d), 1);
+        tc_fence_after();
+#ifdef KO_DRAIN
+        if (d - 1 >= sg.A) release(d - 1);
+        return;
+#endif
+        const int slot = d % 3;
+        uint32_t r[3][16];
+        long long gr[3];
+        bool ok[3];
+        int sxr[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int xr = d - 1 + k;
+          ok[k] = xr >= sg.A && xr < sg.Bn;
+          gr[k] = gx(ok[k] ? xr : d);
+          sxr[k] = sx_s[gr[k] & 7];   // issued before the TMEM loads: the latencies overlap
+        }
+        tmem_ld16x3(tlane + (uint32_t)((gr[0] & 3) * 3 * C + slot * C + c0),
+                    tlane + (uint32_t)((gr[1] & 3) * 3 * C + slot * C + c0),
+                    tlane + (uint32_t)((gr[2] & 3) * 3 * C + slot * C + c0), r);
+        if (warp == 4) TL2(2, gx(d), 5);
+        // the ring of input row d-1 fed rows d-2, d-1, d: free now
+        if (d - 1 >= sg.A) release(d - 1);
+        float f[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) f[k] = ok[k] ? exp2i(-(sxr[k] + sw)) : 0.f;
+        if (warp == 4) TL2(2, gx(d), 2);
+        if (lane_valid) {
+          float *dst = P.out + obase + (size_t)d * P.W;
+#pragma unroll
+          for (int i4 = 0; i4 < HC / 4; ++i4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 4 * i4 + j;
+              // a ring of a row outside the segment may hold stale values:
+              // select, not multiply by zero (0 x inf)
+              float y = bv[i];
+#pragma unroll
+              for (int k = 0; k < 3; ++k) y += ok[k] ? __uint_as_float(r[k][i]) * f[k] : 0.f;
+              if (epi) {
+                if (is_mask) y = e[i] > 0.f ? y : 0.f;
+                else y += e[i];
+              }
+              if (P.relu) y = fmaxf(y, 0.f);
+              dst[(size_t)i * plane] = y;
+            }
+          }
+        }
+        if (warp == 4) TL2(2, gx(d), 3);
+        if (warp == 4) TL2(2, gx(d), 4);
+      };
+      load_epi(sg.R0, ea);
+      int d = sg.R0;
+      for (; d + 1 < sg.R1; d += 2) {
+        drain_row(d, ea, eb);
+        drain_row(d + 1, eb, ea);
+      }
+      if (d < sg.R1) drain_row(d, ea, eb);
+      // rings of the rows below the last output row
+      for (int x = max(sg.A, sg.R1 - 1); x < sg.Bn; ++x) release(x);
+      gbase += sg.Bn - sg.A;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tct2
+#ifdef CT2_TL
+extern "C" int ht_debug_conv2_timeline(long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, tct2::g_ctl2, sizeof(long long) * 3 * 1024 * 6);
+}
+#endif
+
+// true when the shape suits the TMA-staged kernel (16-B row strides, a strip
+// row spans at most two images)
+bool conv_tc2_eligible(int W) { return W % 4 == 0 && W + 1 >= tct2::M; }
+
+int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+                const float *resid, float *out, int relu, cudaStream_t st) {
+  using namespace tct2;
+  HT_REQUIRE(conv_tc2_eligible(W), "conv_tc2: unsupported width %d", W);
+  HT_REQUIRE(!(mask && resid), "conv_tc2: a ReLU mask and a residual in one launch");
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel, SMEM)) return rc;
+  int dev = 0, n_sm = 148;
+  HT_CUDA(cudaGetDevice(&dev));
+  HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  Conv2Params p{};
+  p.w = w; p.bias = bias; p.mask = mask; p.resid = resid; p.out = out;
+  p.B = B; p.H = H; p.W = W; p.VW = B * (W + 1); p.relu = relu;
+  p.n_strips = (p.VW + S - 1) / S;
+  const long long total = (long long)p.n_strips * H;
+  long long grid = n_sm;
+  if (total < grid * 8) grid = (total + 7) / 8;
+  if (grid < 1) grid = 1;
+  p.chunk = (total + grid - 1) / grid;
+  grid = (total + p.chunk - 1) / p.chunk;
+  auto enc = tensor_map_encoder();
+  HT_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t row = (cuuint64_t)W * 4, planeb = row * H;
+  cuuint64_t dims[4] = {(cuuint64_t)W, (cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {planeb, row, planeb * C};
+  cuuint32_t box[4] = {(cuuint32_t)BOXW, (cuuint32_t)C, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(&p.tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HT_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  conv_tc2_kernel<<<(unsigned)grid, NTHR, SMEM, st>>>(p);
+  count_launch();
+  HT_CHECK_LAUNCH();
+  return HT_OK;
+}
+
+}  // namespace ht

@@ -1,5 +1,7 @@
-"""The tcgen05 training convolution (csrc/conv_tc.cu) against the fp32 SIMT
-kernel and a float64 reference, one conv at a time, every epilogue option."""
+"""The tcgen05 training convolutions (csrc/conv_tc2.cu: scaled fp16 pairs, the
+default where the shape allows TMA staging; csrc/conv_tc.cu: split bf16)
+against the fp32 SIMT kernel and a float64 reference, one conv at a time,
+every epilogue option."""
 
 import numpy as np
 import pytest
@@ -41,7 +43,8 @@ def _run(impl, x, w, bias=None, mask=None, resid=None, relu=0):
                                    # tracking across strips), single-row images
                                    (8, 3, 128), (5, 2, 252), (4, 1, 128)])
 @pytest.mark.parametrize("mode", ["plain", "bias_relu", "mask", "resid"])
-def test_conv_tc_matches_reference(B, H, W, mode):
+@pytest.mark.parametrize("impl", [0, 2, 3])
+def test_conv_tc_matches_reference(B, H, W, mode, impl):
     r = Rng(B * 1000 + H * 10 + W)
     x = r.gaussians(B * 32 * H * W).reshape(B, 32, H, W).astype(np.float32).astype(np.float64)
     w = (r.gaussians(32 * 32 * 9).reshape(32, 32, 3, 3) * 0.1).astype(np.float32).astype(np.float64)
@@ -59,9 +62,34 @@ def test_conv_tc_matches_reference(B, H, W, mode):
         rs = r.gaussians(x.size).reshape(x.shape).astype(np.float32).astype(np.float64)
         kw = dict(resid=rs)
         ref = ref + rs
-    tc = _run(0, x, w, **kw)
+    tc = _run(impl, x, w, **kw)
     simt = _run(1, x, w, **kw)
     scale = np.abs(_conv64(np.abs(x), np.abs(w))).max()
     assert np.max(np.abs(simt - ref)) <= 1e-5 * scale
-    # split-bf16 with short accumulation chains: ~1e-7 of scale (SIMT ~2e-7)
+    # split bf16 / scaled fp16 pairs with short accumulation chains: ~1e-7 of
+    # scale (SIMT ~2e-7)
     assert np.max(np.abs(tc - ref)) <= 1e-6 * scale, np.unravel_index(np.argmax(np.abs(tc - ref)), ref.shape)
+
+
+@pytest.mark.parametrize("xscale,wscale", [(1.0, 1.0), (1e-9, 1.0), (1e6, 1e-3), (1e-12, 1e-3)])
+def test_conv_tc2_row_scales(xscale, wscale):
+    """The fp16-pair kernel scales every input row by its own power of two:
+    inputs far outside fp16's range (the backward pass's 1e-9 gradients) and
+    rows whose magnitudes differ by 1e12 keep the fp32-class error per row."""
+    B, H, W = 3, 24, 256
+    r = Rng(77)
+    x = r.gaussians(B * 32 * H * W).reshape(B, 32, H, W)
+    rowmag = 10.0 ** r.uniforms(B * H).reshape(B, 1, H, 1) * 1e-6 ** r.uniforms(B * H).reshape(B, 1, H, 1)
+    x = (x * rowmag * xscale).astype(np.float32).astype(np.float64)
+    w = (r.gaussians(32 * 32 * 9).reshape(32, 32, 3, 3) * 0.1 * wscale).astype(np.float32).astype(np.float64)
+    ref = _conv64(x, w)
+    tc = _run(3, x, w)
+    # error bound per output row: the scale of the three input rows it reads
+    sc = _conv64(np.abs(x), np.abs(w))
+    rows = np.abs(x).max(axis=(1, 3))                         # (B, H)
+    rp = np.pad(rows, ((0, 0), (1, 1)))
+    near = np.maximum(np.maximum(rp[:, :-2], rp[:, 1:-1]), rp[:, 2:])
+    bound = 1e-6 * np.maximum(sc.max(axis=(1, 3)), near * np.abs(w).sum(axis=(1, 2, 3)).max())
+    err = np.abs(tc - ref).max(axis=(1, 3))
+    assert np.all(np.isfinite(tc))
+    assert np.all(err <= bound), float((err / bound).max())
