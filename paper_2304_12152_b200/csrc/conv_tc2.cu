@@ -414,7 +414,13 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (!epi || !(row < sg.R1 && lane_valid)) return;
         const float *src = epi + obase + (size_t)row * P.W;
 #pragma unroll
-        for (int i = 0; i < HC; ++i) e[i] = __ldg(src + (size_t)i * plane);
+        for (int i = 0; i < HC; ++i) {
+#ifdef V_CG
+          e[i] = __ldcg(src + (size_t)i * plane);
+#else
+          e[i] = __ldg(src + (size_t)i * plane);
+#endif
+        }
       };
       auto drain_row = [&](int d, const float (&e)[HC], float (&e_next)[HC]) {
         load_epi(d + 1, e_next);
@@ -473,6 +479,9 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
                 else y += e[i];
               }
               if (P.relu) y = fmaxf(y, 0.f);
+#ifdef V_NOST
+              if (y == 123.456f)
+#endif
               dst[(size_t)i * plane] = y;
             }
           }
