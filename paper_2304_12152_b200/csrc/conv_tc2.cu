@@ -422,8 +422,26 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
 #endif
         }
       };
+      // output row awaiting its stores: issued after the next row's epilogue
+      // loads, so those never queue behind them
+      float y[HC];
+      size_t pend = ~(size_t)0;
+      auto flush = [&]() {
+        if (pend != ~(size_t)0) {
+          float *dst = P.out + pend;
+#pragma unroll
+          for (int i = 0; i < HC; ++i) {
+#ifdef V_NOST
+            if (y[i] == 123.456f)
+#endif
+            dst[(size_t)i * plane] = y[i];
+          }
+          pend = ~(size_t)0;
+        }
+      };
       auto drain_row = [&](int d, const float (&e)[HC], float (&e_next)[HC]) {
         load_epi(d + 1, e_next);
+        flush();
         // MMAs of input rows d-1, d, d+1 done (two issuer warps: no order
         // between their commits, so each is waited for)
         if (warp == 4) TL2(2, gx(d), 0);
@@ -441,51 +459,39 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         return;
 #endif
         const int slot = d % 3;
-        uint32_t r[3][16];
-        long long gr[3];
-        bool ok[3];
         int sxr[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const int xr = d - 1 + k;
-          ok[k] = xr >= sg.A && xr < sg.Bn;
-          gr[k] = gx(ok[k] ? xr : d);
-          sxr[k] = sx_s[gr[k] & 7];   // issued before the TMEM loads: the latencies overlap
+          const int xr = min(max(d - 1 + k, sg.A), sg.Bn - 1);
+          sxr[k] = sx_s[gx(xr) & 7];
         }
-        tmem_ld16x3(tlane + (uint32_t)((gr[0] & 3) * 3 * C + slot * C + c0),
-                    tlane + (uint32_t)((gr[1] & 3) * 3 * C + slot * C + c0),
-                    tlane + (uint32_t)((gr[2] & 3) * 3 * C + slot * C + c0), r);
+#pragma unroll
+        for (int i = 0; i < HC; ++i) y[i] = bv[i];
+        // the three rings one at a time (16 registers), each unscaled exactly;
+        // a ring of a row outside the segment holds stale values: skipped
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int xr = d - 1 + k;
+          if (xr < sg.A || xr >= sg.Bn) continue;
+          float r[HC];
+          tmem_ld16(tlane + (uint32_t)((gx(xr) & 3) * 3 * C + slot * C + c0), r);
+          const float f = exp2i(-(sxr[k] + sw));
+#pragma unroll
+          for (int i = 0; i < HC; ++i) y[i] = fmaf(r[i], f, y[i]);
+        }
         if (warp == 4) TL2(2, gx(d), 5);
         // the ring of input row d-1 fed rows d-2, d-1, d: free now
         if (d - 1 >= sg.A) release(d - 1);
-        float f[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) f[k] = ok[k] ? exp2i(-(sxr[k] + sw)) : 0.f;
         if (warp == 4) TL2(2, gx(d), 2);
-        if (lane_valid) {
-          float *dst = P.out + obase + (size_t)d * P.W;
 #pragma unroll
-          for (int i4 = 0; i4 < HC / 4; ++i4) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int i = 4 * i4 + j;
-              // a ring of a row outside the segment may hold stale values:
-              // select, not multiply by zero (0 x inf)
-              float y = bv[i];
-#pragma unroll
-              for (int k = 0; k < 3; ++k) y += ok[k] ? __uint_as_float(r[k][i]) * f[k] : 0.f;
-              if (epi) {
-                if (is_mask) y = e[i] > 0.f ? y : 0.f;
-                else y += e[i];
-              }
-              if (P.relu) y = fmaxf(y, 0.f);
-#ifdef V_NOST
-              if (y == 123.456f)
-#endif
-              dst[(size_t)i * plane] = y;
-            }
+        for (int i = 0; i < HC; ++i) {
+          if (epi) {
+            if (is_mask) y[i] = e[i] > 0.f ? y[i] : 0.f;
+            else y[i] += e[i];
           }
+          if (P.relu) y[i] = fmaxf(y[i], 0.f);
         }
+        if (lane_valid) pend = obase + (size_t)d * P.W;
         if (warp == 4) TL2(2, gx(d), 3);
         if (warp == 4) TL2(2, gx(d), 4);
       };
@@ -496,6 +502,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         drain_row(d + 1, eb, ea);
       }
       if (d < sg.R1) drain_row(d, ea, eb);
+      flush();
       // rings of the rows below the last output row
       for (int x = max(sg.A, sg.R1 - 1); x < sg.Bn; ++x) release(x);
       gbase += sg.Bn - sg.A;
