@@ -99,3 +99,73 @@ def halftone_page_strip(net, page, noise, group=None, output="h"):
     h = torch.empty((1, st.out_rows, W), dtype=torch.uint8, device=dev)
     net.halftone_device(c, z, h_out=h, rows=st.as_kernel_rows(H), check=True)
     return st, h[0].cpu().numpy()
+
+
+class PageEngine:
+    """Streams pages of one size (H, W) through this rank's row strip
+    (config 4): host contone + noise pages (float32, pinned for asynchronous
+    copies) in, the strip's uint8 halftone rows (1 = white) out.  Each
+    submitted page runs H2D -> fused forward -> D2H on the stream of one of
+    `depth` device-buffer sets, so page i+1's copies overlap page i's
+    kernels; wait() blocks until a page's rows are in its out_host."""
+
+    def __init__(self, net, H, W, group=None, depth=2):
+        import torch
+        from . import _lib
+        _lib.require_cuda()
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.net, self.H, self.W = net, H, W
+        rank, world = dist_info(group)
+        self.strip = st = row_strip(H, rank, world, halo=receptive_radius(net.blocks))
+        dev = net.device
+        self.dev = dev
+        self._sets = [{"stream": torch.cuda.Stream(dev, priority=-1),
+                       "c": torch.empty((1, st.in_rows, W), dtype=torch.float32, device=dev),
+                       "z": torch.empty((1, st.in_rows, W), dtype=torch.float32, device=dev),
+                       "h": torch.empty((1, st.out_rows, W), dtype=torch.uint8, device=dev),
+                       "ws": None} for _ in range(depth)]
+        self._next = 0
+        net.sync()
+
+    def out_shape(self):
+        return (self.strip.out_rows, self.W)
+
+    def h2d_bytes(self):
+        return 2 * self.strip.in_rows * self.W * 4
+
+    def d2h_bytes(self):
+        return self.strip.out_rows * self.W
+
+    def submit(self, page, noise, out_host):
+        """Enqueue one page: page / noise (H, W) float32 CPU tensors (pinned
+        for overlap), out_host (out_rows, W) uint8 CPU tensor; returns a
+        ticket for wait().  Inputs must stay unchanged and out_host unread
+        until then."""
+        import torch
+        st, s = self.strip, self._sets[self._next % len(self._sets)]
+        self._next += 1
+        if tuple(page.shape) != (self.H, self.W) or tuple(noise.shape) != (self.H, self.W):
+            raise ValueError(f"page and noise must be ({self.H}, {self.W})")
+        stream = s["stream"]
+        stream.wait_stream(torch.cuda.current_stream(self.dev))
+        r0, r1 = st.in_row0, st.in_row0 + st.in_rows
+        with torch.cuda.stream(stream):
+            s["c"][0].copy_(page[r0:r1], non_blocking=True)
+            s["z"][0].copy_(noise[r0:r1], non_blocking=True)
+            s["ws"] = self.net.halftone_device(s["c"], s["z"], h_out=s["h"], rows=st.as_kernel_rows(self.H),
+                                               workspace=s["ws"], stream=stream)
+            out_host.copy_(s["h"][0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return (ev, s)
+
+    def wait(self, ticket):
+        """Block until a submitted page's rows are in its out_host.  Raises
+        FloatingPointError if the fused kernel saw a non-finite logit."""
+        import torch
+        from . import _lib
+        ev, s = ticket
+        torch.cuda.current_stream(self.dev).wait_event(ev)
+        ev.synchronize()
+        _lib.call("ht_halftone_check", _lib.ptr(s["ws"]), _lib.stream_ptr(s["stream"]))

@@ -141,6 +141,44 @@ def test_config4_page_row_strips_bitwise():
         _check_window(net, page, z, pf, hf, y0, x0)
 
 
+def test_page_engine_streams_pages(monkeypatch):
+    """parallel.PageEngine: pages streamed two deep (distinct contents per
+    page) give the same rows as one device-path call per page, and the
+    engines of 3 ranks (dist_info monkeypatched) stitch to the whole page."""
+    import torch
+    from paper_2304_12152_b200 import parallel
+    from paper_2304_12152_b200.imagecore import gaussian_noise_map_device
+    net = _net()
+    H, W = 700, 512
+    pages = [synth.contone(H, W, seed=10 + k, blobs=6, rects=2).astype(np.float32) for k in range(3)]
+    noises = [gaussian_noise_map_device(Rng(20 + k), W, H).cpu() for k in range(3)]
+    refs = []
+    for pg, zn in zip(pages, noises):
+        h = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
+        net.halftone_device(torch.from_numpy(pg).cuda()[None], zn.cuda()[None], h_out=h, check=True)
+        refs.append(h[0].cpu())
+    ph = [torch.from_numpy(pg).pin_memory() for pg in pages]
+    zh = [zn.pin_memory() for zn in noises]
+    eng = parallel.PageEngine(net, H, W, depth=2)
+    outs = [torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory() for _ in range(5)]
+    tickets = [eng.submit(ph[i % 3], zh[i % 3], outs[i]) for i in range(2)]
+    for i in range(2, 5):
+        eng.wait(tickets[i - 2])
+        tickets.append(eng.submit(ph[i % 3], zh[i % 3], outs[i]))
+    for t_ in tickets[-2:]:
+        eng.wait(t_)
+    for i in range(5):
+        assert torch.equal(outs[i], refs[i % 3]), i
+    stitched = torch.empty((H, W), dtype=torch.uint8)
+    for rank in range(3):
+        monkeypatch.setattr(parallel, "dist_info", lambda group=None, r=rank: (r, 3))
+        e = parallel.PageEngine(net, H, W, depth=1)
+        o = torch.empty(e.out_shape(), dtype=torch.uint8).pin_memory()
+        e.wait(e.submit(ph[1], zh[1], o))
+        stitched[e.strip.out_row0:e.strip.out_row0 + e.strip.out_rows] = o
+    assert torch.equal(stitched, refs[1])
+
+
 def test_config5_data_parallel_gradient_full_size(monkeypatch):
     """16 x 256^2 + 4 gray, LE + anisotropy: two data-parallel shards (run one
     after the other on this GPU, all-reduce replaced by a host sum) give the
