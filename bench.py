@@ -511,10 +511,13 @@ def bench_cfg5(D, steps, warmup, burst):
 
     with ClockSampler(D.dev.index) as clk:
         ms = timed(D, step, steps, warmup)
-    # tensor work of the 32->32 convs: forward, input gradient, weight
-    # gradient, each as six bf16 products of the three-way split operands
+    # tensor work the 32->32 convs execute per step (default kernels): the
+    # 16 forward conv1s as three fp16-pair products (conv_tc2), the 16 forward
+    # conv2s and the 32 input gradients as six split-bf16 products (conv_tc),
+    # the 32 weight gradients as three two-part bf16 products (wgrad_tc)
     px = 20 * 256 * 256
-    flop = px * 2 * 9 * 32 * 32 * 32 * 3 * 6
+    products = 16 * 3 + 16 * 6 + 32 * 6 + 32 * 3
+    flop = px * 2 * 9 * 32 * 32 * products
     return {"workload": "BASELINE config 5: train_step, 16 x 256x256 crops + 4 flat-gray images, "
                         "LE estimator (Gaussian HVS), anisotropy loss, backward, Adam",
             "value": round(1e3 / ms, 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
@@ -522,7 +525,7 @@ def bench_cfg5(D, steps, warmup, burst):
             "roofline": {"bound": "tensor", "unit": "TFLOP/s",
                          "achieved": round(flop / (ms * 1e-3) / 1e12, 1), "peak": burst,
                          "frac": round(flop / (ms * 1e-3) / 1e12 / burst, 4),
-                         "work": "32->32 convs (fwd + dgrad + wgrad) x 6 split-bf16 products, whole step time"},
+                         "work": "executed MMA work of the 32->32 convs (fwd conv1 3 fp16-pair products, fwd conv2 and dgrad 6 split-bf16, wgrad 3 two-part bf16) over the whole step time"},
             "last_diag": {k: (round(v, 9) if isinstance(v, float) else v) for k, v in diag.items()},
             "clocks": clk.summary()}
 
