@@ -137,10 +137,10 @@ int ht_timing_read(int *tags, float *ms, int max, int *count);
 
 /* Training convolutions (nn.py:46-77): 0 = the 32 -> 32 convs of the residual
  * blocks (forward, input gradient and weight gradient) on tcgen05 (default:
- * scaled fp16 pairs for convs without a mask / residual input, split-bf16
- * operands for the rest), 1 = fp32 SIMT kernels only (cross-check), 2 =
- * tcgen05 with split-bf16 operands everywhere, 3 = tcgen05 with scaled fp16
- * pairs wherever the shape allows.  Process-wide. */
+ * scaled fp16 pairs where the shape allows TMA staging, W % 4 == 0 and
+ * W >= 127; split-bf16 operands otherwise), 1 = fp32 SIMT kernels only
+ * (cross-check), 2 = tcgen05 with split-bf16 operands everywhere, 3 = same
+ * as 0.  Process-wide. */
 int ht_set_train_conv_impl(int impl);
 /* bf16 parts of the tensor-core weight gradient: 2 (three products,
  * ~2^-16 per product; default -- the config-5 step stays at 1.6e-5 of the

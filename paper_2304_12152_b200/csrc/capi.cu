@@ -187,10 +187,9 @@ int ht_timing_read(int *tags, float *ms, int max, int *count) {
 }
 
 // Training convolutions: 0 = tcgen05 kernels for the 32 -> 32 convs
-// (default; scaled fp16 pairs for launches without a mask / residual input,
-// split bf16 for the rest), 1 = fp32 SIMT kernels only (cross-check), 2 =
-// tcgen05 with the split-bf16 conv everywhere, 3 = tcgen05 with the fp16-pair
-// conv wherever the shape allows.
+// (default; scaled fp16 pairs where the shape allows TMA staging, split bf16
+// otherwise), 1 = fp32 SIMT kernels only (cross-check), 2 = tcgen05 with the
+// split-bf16 conv everywhere, 3 = same as 0.
 int ht_set_train_conv_impl(int impl) {
   if (impl < 0 || impl > 3) return ht::fail(HT_E_INVALID, "impl must be 0 (tensor core), 1 (simt), 2 (split bf16) or 3 (fp16 pairs)");
   ht::g_train_conv_impl = impl;

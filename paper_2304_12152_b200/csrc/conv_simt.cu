@@ -330,10 +330,10 @@ int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *
 bool conv_tc2_eligible(int W);
 int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
                 const float *resid, float *out, int relu, cudaStream_t st);
-// 0: tensor cores for 32 -> 32 convs (default: conv_tc2 for launches without
-// a mask / residual input, conv_tc otherwise), 1: SIMT only, 2: tensor cores
-// with conv_tc.cu's split-bf16 kernel everywhere, 3: conv_tc2 wherever the
-// shape allows (A/B and tests)
+// 0: tensor cores for 32 -> 32 convs (default: conv_tc2 where the shape
+// allows TMA staging, conv_tc otherwise), 1: SIMT only, 2: tensor cores with
+// conv_tc.cu's split-bf16 kernel everywhere, 3: same as 0 (kept for A/B
+// scripts)
 extern int g_train_conv_impl;
 // wgrad_tc.cu: their weight gradient on tcgen05 (split-bf16, `parts` bf16 parts)
 int wgrad_tc32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int parts,
@@ -345,12 +345,9 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
                     const float *mask, const float *resid, float *out, int relu,
                     cudaStream_t st) {
   if constexpr (CIN == 32 && COUT == 32) {
-    // conv_tc2 where it measured faster: launches without a mask / residual
-    // input (the forward conv1s; 20 x 256^2: 115 vs 134 us).  With one, its
-    // drainers wait on the input's loads (175 vs 161 us), so conv_tc runs those.
-    if (g_train_conv_impl == 0 && conv_tc2_eligible(W) && !mask && !resid)
-      return conv_tc2_32(x, B, H, W, w, bias, mask, resid, out, relu, st);
-    if (g_train_conv_impl == 3 && conv_tc2_eligible(W) && !(mask && resid))
+    // conv_tc2 (20 x 256^2: 110 vs 134 us plain, 143 vs 162 us with a mask
+    // or residual input) wherever the shape allows TMA staging
+    if ((g_train_conv_impl == 0 || g_train_conv_impl == 3) && conv_tc2_eligible(W) && !(mask && resid))
       return conv_tc2_32(x, B, H, W, w, bias, mask, resid, out, relu, st);
     if (g_train_conv_impl != 1) return conv_tc32(x, B, H, W, w, bias, mask, resid, out, relu, st);
   }

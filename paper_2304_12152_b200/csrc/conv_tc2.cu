@@ -50,28 +50,38 @@ constexpr int PLANE = M * 16;             // 8 channels x 128 lanes (fp16)
 constexpr int ROW = 4 * PLANE;            // 32 channels of a row, one part
 constexpr int TILE = 2 * NSL * C * 16;    // B tile (kx, K-half): 160 rows x 2 K-chunks x 16 B
 constexpr int W_BYTES = NPART * 6 * TILE;
-constexpr int NAB = 3;                    // A buffers
 constexpr int A_OFF = W_BYTES;
-constexpr int A_BYTES = NAB * NPART * ROW;
-constexpr int NSTG = 3;                   // staging slots (TMA three rows ahead)
 constexpr int BOXW = M + 4;               // box: 132 px x 32 channels fp32, [ch][px]
 constexpr int BOX = BOXW * C * 4;
 constexpr int STG_SLOT = 2 * BOX;         // a strip row spans at most two images
-constexpr int STG_OFF = A_OFF + A_BYTES;
-constexpr int BAR_OFF = STG_OFF + NSTG * STG_SLOT;
 constexpr int NRING = 4;                  // TMEM rings of 96 columns
-// barriers (8 B each): acc_full[4], ready[4], ring_free[4], stg_full[3], stg_empty[3]
-constexpr int B_ACC = 0, B_RDY = 4, B_FREE = 8, B_STG = 12, B_STE = 15, NBARS = 18;
-constexpr int MISC_OFF = BAR_OFF + NBARS * 8;   // tmem slot, pad, sx[8], red[2][8], wred[24]
-constexpr int SMEM = MISC_OFF + 384;
+// barriers (8 B each): acc_full[4], ready[4], ring_free[4], stg_full[<=3],
+// stg_empty[<=3], epi_full[2], epi_empty[2]
+constexpr int B_ACC = 0, B_RDY = 4, B_FREE = 8, B_STG = 12, B_STE = 15, B_EF = 18, B_EE = 20, NBARS = 22;
+// Shared-memory layout.  Without an epilogue input: three A buffers and
+// three staging slots (TMA three rows ahead); with one, its rows take two
+// staging slots of their own and the others drop to two each (227 KB).
+template <bool EPI>
+struct Lay2 {
+  static constexpr int NAB = EPI ? 2 : 3;     // A buffers
+  static constexpr int NSTG = EPI ? 2 : 3;    // input-row staging slots
+  static constexpr int NESTG = EPI ? 2 : 0;   // epilogue-input (mask / residual) row slots
+  static constexpr int A_BYTES = NAB * NPART * ROW;
+  static constexpr int STG_OFF = A_OFF + A_BYTES;
+  static constexpr int ESTG_OFF = STG_OFF + NSTG * STG_SLOT;
+  static constexpr int BAR_OFF = ESTG_OFF + NESTG * STG_SLOT;
+  static constexpr int MISC_OFF = BAR_OFF + NBARS * 8;   // tmem slot, pad, sx[8], red[2][8], wred[24]
+  static constexpr int SMEM = MISC_OFF + 384;
+  static_assert(STG_OFF % 1024 == 0 && ESTG_OFF % 1024 == 0 && BOX % 128 == 0,
+                "TMA destinations must stay 128-B aligned");
+  static_assert(SMEM <= 232448, "shared memory exceeded");
+};
 constexpr int NSPL = 128, NDRN = 256;
 constexpr int NISS = 2;                         // MMA issuer warps (even / odd rows)
-constexpr int NTHR = NSPL + NDRN + 32 * NISS + 32;   // + issuers + TMA producer warp
+constexpr int NTHR = NSPL + NDRN + 32 * NISS + 64;   // + issuers + two TMA producer warps
 constexpr int HC = C / 2;
 constexpr int SCALE_TOP = 14;             // scaled max |x| in [2^(SCALE_TOP-1), 2^SCALE_TOP)
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-static_assert(STG_OFF % 1024 == 0 && BOX % 128 == 0, "TMA destinations must stay 128-B aligned");
-static_assert(SMEM <= 232448, "shared memory exceeded");
 __constant__ int c_ky2[NSL] = {2, 1, 0, 2, 1};
 
 __device__ __forceinline__ float exp2i(int e) { return __int_as_float((127 + e) << 23); }
@@ -130,6 +140,8 @@ __device__ long long g_ctl2[3][1024][6];
 
 struct Conv2Params {
   CUtensorMap tm_x;   // x as (W, C, H, B) fp32, box 132 x 32 x 1 x 1
+  CUtensorMap tm_e;   // the mask or residual, same geometry (when has_epi)
+  int has_epi, is_mask;
   const float *w, *bias, *mask, *resid;
   float *out;
   int B, H, W, VW, relu;
@@ -151,7 +163,12 @@ __device__ __forceinline__ long long next_seg(long long qq, long long q1, int H,
   return end;
 }
 
+template <bool EPI>
 __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant__ Conv2Params P) {
+  using L = Lay2<EPI>;
+  constexpr int NAB = L::NAB, NSTG = L::NSTG, NESTG = EPI ? L::NESTG : 1;
+  constexpr int A_BYTES = L::A_BYTES, STG_OFF = L::STG_OFF, ESTG_OFF = L::ESTG_OFF;
+  constexpr int BAR_OFF = L::BAR_OFF, MISC_OFF = L::MISC_OFF;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -162,6 +179,8 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   auto ring_free = [&](long long g) { return bar(B_FREE + (int)(g & 3)); };
   auto stg_full = [&](long long g) { return bar(B_STG + (int)(g % NSTG)); };
   auto stg_empty = [&](long long g) { return bar(B_STE + (int)(g % NSTG)); };
+  auto epi_full = [&](long long g) { return bar(B_EF + (int)(g % NESTG)); };
+  auto epi_empty = [&](long long g) { return bar(B_EE + (int)(g % NESTG)); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + MISC_OFF);
   int *sx_s = reinterpret_cast<int *>(smem + MISC_OFF + 8);        // [8] row scale by g & 7
   int *red = reinterpret_cast<int *>(smem + MISC_OFF + 48);        // [2][8] row-max partials
@@ -176,6 +195,10 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     for (int k = 0; k < NSTG; ++k) {
       mbar_init(bar(B_STG + k), 1);
       mbar_init(bar(B_STE + k), NSPL / 32);
+    }
+    for (int k = 0; k < L::NESTG; ++k) {
+      mbar_init(bar(B_EF + k), 1);
+      mbar_init(bar(B_EE + k), NDRN / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -224,7 +247,26 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * P.H);
   const int WP = P.W + 1;
 
-  if (warp == (NSPL + NDRN) / 32 + NISS) {
+  if (warp == (NSPL + NDRN) / 32 + NISS + 1) {
+    // ================= producer: epilogue-input rows (mask / residual) ======
+    if (lane == 0 && EPI) {
+      long long ge = 0;
+      for (long long qq = q0; qq < q1;) {
+        Seg sg;
+        qq = next_seg(qq, q1, P.H, sg);
+        const int v0 = sg.s * S - 1, b0 = max(v0, 0) / WP;
+        const int nbox = (b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
+        const int c0a = (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
+        for (int d = sg.R0; d < sg.R1; ++d, ++ge) {
+          if (ge >= NESTG) mbar_wait(epi_empty(ge), (uint32_t)((ge / NESTG) - 1) & 1u);
+          const uint32_t fb = epi_full(ge), dst = sbase + ESTG_OFF + (uint32_t)(ge % NESTG) * STG_SLOT;
+          mbar_expect_tx(fb, nbox * BOX);
+          tma_load_4d(dst, &P.tm_e, c0a, 0, d, b0, fb);
+          if (nbox == 2) tma_load_4d(dst + BOX, &P.tm_e, c0b, 0, d, b0 + 1, fb);
+        }
+      }
+    }
+  } else if (warp == (NSPL + NDRN) / 32 + NISS) {
     // ================= producer: input rows by TMA, NSTG rows ahead ========
     if (lane == 0) {
       long long tg = 0;
@@ -386,16 +428,14 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16);
     const int l = wq * 32 + lane, c0 = half * HC;
     // the one epilogue input of a launch (the training path passes a ReLU
-    // mask or a residual, never both: conv_tc2_32 requires that), two row
-    // buffers: row d+1's loads are issued before row d's drain, a whole row
-    // period ahead of their use, with no register copy in between
+    // mask or a residual, never both: conv_tc2_32 requires that) arrives by
+    // TMA, two output rows ahead, in the epilogue staging ring
     float bv[HC];
 #pragma unroll
     for (int i = 0; i < HC; ++i) bv[i] = P.bias ? __ldg(P.bias + c0 + i) : 0.f;
-    const float *epi = P.mask ? P.mask : P.resid;
-    const bool is_mask = P.mask != nullptr;
-    float ea[HC], eb[HC];
-    long long gbase = 0;
+    constexpr bool has_epi = EPI;
+    const bool is_mask = P.is_mask != 0;
+    long long gbase = 0, ge = 0;
     for (long long qq = q0; qq < q1;) {
       Seg sg;
       qq = next_seg(qq, q1, P.H, sg);
@@ -404,23 +444,16 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       const bool in_img = v >= 0 && v < P.VW && col < P.W;
       const bool lane_valid = l >= 1 && l < 1 + S && in_img;
       const size_t obase = ((size_t)b * C + c0) * plane + col;
+      // this lane's column in the staged epilogue boxes (as the splitters')
+      const int eb0 = max(sg.s * S - 1, 0) / WP;
+      const int ekbox = in_img ? b - eb0 : -1;
+      const int ekcol = (sg.s * S - 1) - (eb0 + max(ekbox, 0)) * WP;
+      const int ekoff = max(ekbox, 0) * (BOX / 4) + l + (ekcol & 3) + c0 * BOXW;
       auto gx = [&](int x) { return gbase + (x - sg.A); };
       auto release = [&](int x) {   // ring of input row x: every output row it feeds is drained
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ring_free(gx(x)));
-      };
-      auto load_epi = [&](int row, float (&e)[HC]) {
-        if (!epi || !(row < sg.R1 && lane_valid)) return;
-        const float *src = epi + obase + (size_t)row * P.W;
-#pragma unroll
-        for (int i = 0; i < HC; ++i) {
-#ifdef V_CG
-          e[i] = __ldcg(src + (size_t)i * plane);
-#else
-          e[i] = __ldg(src + (size_t)i * plane);
-#endif
-        }
       };
       // output row awaiting its stores: issued after the next row's epilogue
       // loads, so those never queue behind them
@@ -439,8 +472,20 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
           pend = ~(size_t)0;
         }
       };
-      auto drain_row = [&](int d, const float (&e)[HC], float (&e_next)[HC]) {
-        load_epi(d + 1, e_next);
+      auto drain_row = [&](int d) {
+        float e[HC];
+        if (has_epi) {
+          // this row's mask / residual from its staging slot; the slot is
+          // released at once (the arrive orders the reads before it)
+          if (lane == 0) mbar_wait(epi_full(ge), (uint32_t)(ge / NESTG) & 1u);
+          __syncwarp();
+          const float *src = reinterpret_cast<const float *>(smem + ESTG_OFF + (uint32_t)(ge % NESTG) * STG_SLOT) + ekoff;
+#pragma unroll
+          for (int i = 0; i < HC; ++i) e[i] = src[i * BOXW];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(epi_empty(ge));
+        }
+        ++ge;
         flush();
         // MMAs of input rows d-1, d, d+1 done (two issuer warps: no order
         // between their commits, so each is waited for)
@@ -485,7 +530,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (warp == 4) TL2(2, gx(d), 2);
 #pragma unroll
         for (int i = 0; i < HC; ++i) {
-          if (epi) {
+          if (has_epi) {
             if (is_mask) y[i] = e[i] > 0.f ? y[i] : 0.f;
             else y[i] += e[i];
           }
@@ -495,13 +540,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (warp == 4) TL2(2, gx(d), 3);
         if (warp == 4) TL2(2, gx(d), 4);
       };
-      load_epi(sg.R0, ea);
-      int d = sg.R0;
-      for (; d + 1 < sg.R1; d += 2) {
-        drain_row(d, ea, eb);
-        drain_row(d + 1, eb, ea);
-      }
-      if (d < sg.R1) drain_row(d, ea, eb);
+      for (int d = sg.R0; d < sg.R1; ++d) drain_row(d);
       flush();
       // rings of the rows below the last output row
       for (int x = max(sg.A, sg.R1 - 1); x < sg.Bn; ++x) release(x);
@@ -532,7 +571,8 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
   using namespace tct2;
   HT_REQUIRE(conv_tc2_eligible(W), "conv_tc2: unsupported width %d", W);
   HT_REQUIRE(!(mask && resid), "conv_tc2: a ReLU mask and a residual in one launch");
-  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel, SMEM)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<false>, Lay2<false>::SMEM)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<true>, Lay2<true>::SMEM)) return rc;
   int dev = 0, n_sm = 148;
   HT_CUDA(cudaGetDevice(&dev));
   HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
@@ -557,7 +597,17 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   HT_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  conv_tc2_kernel<<<(unsigned)grid, NTHR, SMEM, st>>>(p);
+  const float *epi = mask ? mask : resid;
+  p.has_epi = epi != nullptr;
+  p.is_mask = mask != nullptr;
+  if (epi) {
+    const CUresult re = enc(&p.tm_e, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(epi), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HT_REQUIRE(re == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)re);
+  }
+  if (epi) conv_tc2_kernel<true><<<(unsigned)grid, NTHR, Lay2<true>::SMEM, st>>>(p);
+  else conv_tc2_kernel<false><<<(unsigned)grid, NTHR, Lay2<false>::SMEM, st>>>(p);
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
