@@ -451,10 +451,19 @@ def _prepare_step(dataset, cfg, rng, dev, rank, world):
     rng.jump((bs - hi) * n)
     run_aniso = cfg.w_a != 0.0 and (cfg.levels == 2 or cfg.multitone_anisotropy)
     nm, ng, ba = hi - lo, 0, cfg.anisotropy_batch_size or bs
-    inputs, cd = [], None
+    inputs, cd, ready = [], None, None
     if nm:
-        cd = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory().to(dev, non_blocking=True)
-        inputs.append(torch.stack((cd, noises), dim=1))
+        # the crops' H2D on a copy stream: a prefetch enqueued mid-step must
+        # not sit in the compute stream between this step's kernels; users
+        # of the batch wait for it (_materialize)
+        host = torch.from_numpy(np.stack(crops[lo:hi]).astype(np.float32)).pin_memory()
+        cs = _copy_stream(dev)
+        with torch.cuda.stream(cs):
+            cd = host.to(dev, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(cs)
+        cd.record_stream(torch.cuda.current_stream(dev))
+        inputs.append((cd, noises))
     if run_aniso:
         grays = [rng.uniform() for _ in range(ba)]
         glo, ghi = shard_range(ba, rank, world)
@@ -474,7 +483,31 @@ def _prepare_step(dataset, cfg, rng, dev, rank, world):
             gd = gd.pin_memory().to(dev, non_blocking=True)[:, None, None].expand(-1, size, size)
             inputs.append(torch.stack((gd, znoise), dim=1))
     return {"start": start, "end": rng.state_words(), "rng_at_fwd": rng_at_fwd, "lo": lo, "hi": hi,
-            "nm": nm, "ng": ng, "ba": ba, "cd": cd, "ud": ud, "inputs": inputs}
+            "nm": nm, "ng": ng, "ba": ba, "cd": cd, "ud": ud, "inputs": inputs, "ready": ready}
+
+
+_copy_streams = {}
+
+
+def _copy_stream(dev):
+    torch = _torch()
+    key = str(dev)
+    if key not in _copy_streams:
+        _copy_streams[key] = torch.cuda.Stream(dev)
+    return _copy_streams[key]
+
+
+def _materialize(prep):
+    """Order the current stream after the prepared batch's H2D and build the
+    MARL input planes (contone, noise) on it (once)."""
+    torch = _torch()
+    if prep.get("ready") is not None:
+        torch.cuda.current_stream(prep["cd"].device).wait_event(prep["ready"])
+        prep["ready"] = None
+    if prep["inputs"] and isinstance(prep["inputs"][0], tuple):
+        cd, noises = prep["inputs"][0]
+        prep["inputs"][0] = torch.stack((cd, noises), dim=1)
+    return prep
 
 
 # the next step's draws and inputs, prepared while the GPU runs this step
@@ -515,6 +548,7 @@ def _speculate_forward(net, dev):
     prep = _next_step.get("prep")
     if prep is None or not prep["inputs"]:
         return
+    _materialize(prep)
     # this step's backward has consumed the training cache: free it before the
     # speculative forward allocates its own (no doubled activation memory)
     net._cache = None
@@ -555,7 +589,7 @@ def train_step(net, adam, dataset, cfg, rng, t, group=None, signal_override=None
     dev = net.device
     bs = cfg.batch_size
     mcfg = cfg.metric_config()
-    prep = _take_prepared(dataset, cfg, rng, dev, rank, world)
+    prep = _materialize(_take_prepared(dataset, cfg, rng, dev, rank, world))
     spec = _next_step.pop("spec", None)
     lo, nm, ng, ba = prep["lo"], prep["nm"], prep["ng"], prep["ba"]
     cd, ud, inputs, rng_at_fwd = prep["cd"], prep["ud"], prep["inputs"], prep["rng_at_fwd"]
