@@ -54,10 +54,14 @@ constexpr int A_OFF = W_BYTES;
 constexpr int BOXW = M + 4;               // box: 132 px x 32 channels fp32, [ch][px]
 constexpr int BOX = BOXW * C * 4;
 constexpr int STG_SLOT = 2 * BOX;         // a strip row spans at most two images
-constexpr int NRING = 4;                  // TMEM rings of 96 columns
-// barriers (8 B each): acc_full[4], ready[4], ring_free[4], stg_full[<=3],
-// stg_empty[<=3], epi_full[2], epi_empty[2]
-constexpr int B_ACC = 0, B_RDY = 4, B_FREE = 8, B_STG = 12, B_STE = 15, B_EF = 18, B_EE = 20, NBARS = 22;
+constexpr int NRING = 4;                  // TMEM rings of 96 columns (five measured no faster)
+// barriers (8 B each): acc_full[8], ready[8], ring_free[NRING], stg_full[<=3],
+// stg_empty[<=3], epi_full[2], epi_empty[2].  acc_full / ready are indexed by
+// row & 7 so that no waiter is ever two phases behind its barrier: the two
+// issuer warps wait on alternate rows' ready barriers, and the splitters can
+// run NAB rows past a slow issuer.
+constexpr int NSEQ = 8;
+constexpr int B_ACC = 0, B_RDY = 8, B_FREE = 16, B_STG = 21, B_STE = 24, B_EF = 27, B_EE = 29, NBARS = 32;
 // Shared-memory layout.  Without an epilogue input: three A buffers and
 // three staging slots (TMA three rows ahead); with one, its rows take two
 // staging slots of their own and the others drop to two each (227 KB).
@@ -174,9 +178,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t sbase = smem_u32(smem);
   auto bar = [&](int k) { return sbase + BAR_OFF + 8u * (uint32_t)k; };
-  auto acc_full = [&](long long g) { return bar(B_ACC + (int)(g & 3)); };
-  auto ready = [&](long long g) { return bar(B_RDY + (int)(g & 3)); };
-  auto ring_free = [&](long long g) { return bar(B_FREE + (int)(g & 3)); };
+  auto acc_full = [&](long long g) { return bar(B_ACC + (int)(g % NSEQ)); };
+  auto ready = [&](long long g) { return bar(B_RDY + (int)(g % NSEQ)); };
+  // parity of row g's phase on its acc_full / ready barrier
+  auto seq_par = [](long long g) { return (uint32_t)(g / NSEQ) & 1u; };
+  auto ring_free = [&](long long g) { return bar(B_FREE + (int)(g % NRING)); };
   auto stg_full = [&](long long g) { return bar(B_STG + (int)(g % NSTG)); };
   auto stg_empty = [&](long long g) { return bar(B_STE + (int)(g % NSTG)); };
   auto epi_full = [&](long long g) { return bar(B_EF + (int)(g % NESTG)); };
@@ -187,11 +193,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   int *wred = reinterpret_cast<int *>(smem + MISC_OFF + 112);      // [24] weight-max partials
   float *bias_s = reinterpret_cast<float *>(smem + MISC_OFF + 208); // [32] bias
   if (tid == 0) {
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NSEQ; ++k) {
       mbar_init(bar(B_ACC + k), 1);
       mbar_init(bar(B_RDY + k), NSPL / 32);
-      mbar_init(bar(B_FREE + k), NDRN / 32);
     }
+    for (int k = 0; k < NRING; ++k) mbar_init(bar(B_FREE + k), NDRN / 32);
     for (int k = 0; k < NSTG; ++k) {
       mbar_init(bar(B_STG + k), 1);
       mbar_init(bar(B_STE + k), NSPL / 32);
@@ -307,14 +313,14 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if ((int)(g % NISS) != iss) continue;
         TL2(0, g, 0);
 #ifndef KO_NOWAIT
-        if (lane == 0) mbar_wait(ready(g), (uint32_t)(g >> 2) & 1u);
+        if (lane == 0) mbar_wait(ready(g), seq_par(g));
 #endif
         __syncwarp();
         TL2(0, g, 1);
         TL2(0, g, 2);
         if (g >= NRING) {
 #ifndef KO_NOWAIT
-          if (lane == 0) mbar_wait(ring_free(g), (uint32_t)((g >> 2) - 1) & 1u);
+          if (lane == 0) mbar_wait(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
 #endif
           __syncwarp();
         }
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         tc_fence_after();
         if (lane == 0) {
           const int o = xm3 == 0 ? 1 : (xm3 == 1 ? 0 : 2);   // B window for rows (x+1, x, x-1)
-          const uint32_t d = tmem + (uint32_t)((g & 3) * 3 * C);
+          const uint32_t d = tmem + (uint32_t)((g % NRING) * 3 * C);
           const uint64_t a0 = adesc0 + ((A_OFF + (uint32_t)(g % NAB) * NPART * ROW) >> 4);
           const uint64_t b0 = bdesc0 + ((o * C * 16) >> 4);
           constexpr uint64_t AP = ROW >> 4, BP = (6 * TILE) >> 4, TB = TILE >> 4, KH = (2 * PLANE) >> 4;
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (warp == 0) TL2(1, g, 1);
 #ifdef KO_SPLIT
         if (lane == 0) mbar_arrive(stg_empty(g));
-        if (g >= NAB) { if (lane == 0) mbar_wait(acc_full(g - NAB), (uint32_t)((g - NAB) >> 2) & 1u); __syncwarp(); }
+        if (g >= NAB) { if (lane == 0) mbar_wait(acc_full(g - NAB), seq_par(g - NAB)); __syncwarp(); }
         if (tid == 0) sx_s[g & 7] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(ready(g));
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (warp == 0) TL2(1, g, 2);
         // A buffer g % NAB was last read by MMA(g - NAB)
         if (g >= NAB) {
-          if (lane == 0) mbar_wait(acc_full(g - NAB), (uint32_t)((g - NAB) >> 2) & 1u);
+          if (lane == 0) mbar_wait(acc_full(g - NAB), seq_par(g - NAB));
           __syncwarp();
         }
         if (warp == 0) TL2(1, g, 3);
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (lane == 0) {
           for (int xr = max(d - 1, sg.A); xr <= min(d + 1, sg.Bn - 1); ++xr) {
             const long long gt = gx(xr);
-            mbar_wait(acc_full(gt), (uint32_t)(gt >> 2) & 1u);
+            mbar_wait(acc_full(gt), seq_par(gt));
           }
         }
         __syncwarp();
@@ -519,7 +525,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
           const int xr = d - 1 + k;
           if (xr < sg.A || xr >= sg.Bn) continue;
           float r[HC];
-          tmem_ld16(tlane + (uint32_t)((gx(xr) & 3) * 3 * C + slot * C + c0), r);
+          tmem_ld16(tlane + (uint32_t)((gx(xr) % NRING) * 3 * C + slot * C + c0), r);
           const float f = exp2i(-(sxr[k] + sw));
 #pragma unroll
           for (int i = 0; i < HC; ++i) y[i] = fmaf(r[i], f, y[i]);
