@@ -147,6 +147,10 @@ int ht_set_train_conv_impl(int impl);
  * reference normwise per tensor, tests/test_gpu_train_cfg5.py) or 3 (six
  * products, fp32 level). */
 int ht_set_wgrad_parts(int parts);
+/* Weight gradients of the edge convs (conv_in 2 -> C, conv_out C -> 1,
+ * nn.py:62-77): 0 = warp-per-row kernel reading each input once (default),
+ * 1 = the generic SIMT tile kernel (cross-check).  Process-wide. */
+int ht_set_edge_wgrad_impl(int impl);
 /* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
  * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +
  * bias, zeroed where mask <= 0, + resid, ReLU if relu -- Conv2d.forward

@@ -190,6 +190,144 @@ conv3x3_wgrad_kernel(const float *__restrict__ x, const float *__restrict__ dout
 }
 
 // ---------------------------------------------------------------------------
+// Edge weight gradients (conv_in 2 -> C, conv_out C -> 1; nn.py:62-77): one
+// side has C channels ("many"), the other F = 1 or 2 ("few").  A warp owns one
+// (image, many-channel j, band of rows) and sweeps it row by row: each lane
+// holds 8 columns of the many-channel row and a 3-row x 10-column register
+// window of the few channels, so every input value is read from memory once
+// per warp and the 9 F tap sums stay in registers (reduced over the warp at
+// the end of the band, added in fp64).  dW[(j F + f) 9 + 3 ky + kx]:
+//   S = +1 (conv_in):  many = dout (co = j), few = x    at (y+ky-1, x+kx-1)
+//   S = -1 (conv_out): many = x (ci = j),    few = dout at (y-ky+1, x-kx+1)
+// db: conv_in db[j] = sum of the many rows; conv_out db[0] = sum of the few.
+constexpr int EW_RB = 32;          // rows per warp task (fp32 chain length RB x 256)
+template <int F, int S>
+__global__ void __launch_bounds__(256) edge_wgrad_kernel(const float *__restrict__ many, const float *__restrict__ few,
+                                                         int B, int C, int H, int W, double *__restrict__ dw,
+                                                         double *__restrict__ db) {
+  const int lane = threadIdx.x & 31;
+  const long long wglob = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  const int n_bands = (H + EW_RB - 1) / EW_RB;
+  const long long tasks = (long long)B * C * n_bands;
+  const size_t plane = (size_t)H * W;
+  const bool vec = (W & 7) == 0;
+  for (long long task = wglob; task < tasks; task += nw) {
+    const int band = (int)(task % n_bands), j = (int)((task / n_bands) % C), b = (int)(task / ((long long)n_bands * C));
+    const int y0 = band * EW_RB, y1 = min(H, y0 + EW_RB);
+    float acc[F][9];
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int t = 0; t < 9; ++t) acc[f][t] = 0.f;
+    float dbacc = 0.f;
+    const float *mrow0 = many + ((size_t)b * C + j) * plane;
+    for (int xc = 0; xc < W; xc += 256) {
+      const int x0 = xc + lane * 8;
+      // raw loads of few-channel row yy: the 8 columns x0 .. x0+7 and, for the
+      // chunk's edge lanes, the halo column (zero outside the image); the halo
+      // columns of the other lanes come from their neighbours (widen)
+      auto load_few = [&](int yy, float (&cen)[F][8], float (&edge)[F]) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cen[f][k] = 0.f;
+          edge[f] = 0.f;
+          if (yy < 0 || yy >= H) continue;
+          const float *r = few + ((size_t)b * F + f) * plane + (size_t)yy * W;
+          if (vec && x0 + 8 <= W) {
+            const float4 u = __ldg(reinterpret_cast<const float4 *>(r + x0));
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(r + x0 + 4));
+            cen[f][0] = u.x; cen[f][1] = u.y; cen[f][2] = u.z; cen[f][3] = u.w;
+            cen[f][4] = v.x; cen[f][5] = v.y; cen[f][6] = v.z; cen[f][7] = v.w;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (x0 + k < W) cen[f][k] = __ldg(r + x0 + k);
+          }
+          if (lane == 0 && x0 - 1 >= 0 && x0 - 1 < W) edge[f] = __ldg(r + x0 - 1);
+          if (lane == 31 && x0 + 8 < W) edge[f] = __ldg(r + x0 + 8);
+        }
+      };
+      auto widen = [&](const float (&cen)[F][8], const float (&edge)[F], float (&dst)[F][10]) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dst[f][1 + k] = cen[f][k];
+          const float left = __shfl_up_sync(0xffffffffu, cen[f][7], 1);
+          const float right = __shfl_down_sync(0xffffffffu, cen[f][0], 1);
+          dst[f][0] = lane > 0 ? left : edge[f];
+          dst[f][9] = lane < 31 ? right : edge[f];
+        }
+      };
+      auto load_many = [&](int y, float (&a)[8]) {
+        const float *mr = mrow0 + (size_t)y * W;
+        if (vec && x0 + 8 <= W) {
+          const float4 u = __ldg(reinterpret_cast<const float4 *>(mr + x0));
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(mr + x0 + 4));
+          a[0] = u.x; a[1] = u.y; a[2] = u.z; a[3] = u.w; a[4] = v.x; a[5] = v.y; a[6] = v.z; a[7] = v.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = x0 + k < W ? __ldg(mr + x0 + k) : 0.f;
+        }
+      };
+      float w0[F][10], w1[F][10], w2[F][10];   // few rows y-1, y, y+1
+      float nc[F][8], ne[F], a[8];
+      load_few(y0 - 1, nc, ne);
+      widen(nc, ne, w0);
+      load_few(y0, nc, ne);
+      widen(nc, ne, w1);
+      for (int y = y0; y < y1; ++y) {
+        load_few(y + 1, nc, ne);
+        load_many(y, a);
+        widen(nc, ne, w2);
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky) {
+            // window row of tap ky: S = +1 -> y + ky - 1, S = -1 -> y - ky + 1
+            const float(&wr)[10] = (S > 0 ? ky : 2 - ky) == 0 ? w0[f] : ((S > 0 ? ky : 2 - ky) == 1 ? w1[f] : w2[f]);
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+              const int c = S > 0 ? kx : 2 - kx;   // column offset into the window
+              float s = acc[f][ky * 3 + kx];
+#pragma unroll
+              for (int p = 0; p < 8; ++p) s = fmaf(a[p], wr[p + c], s);
+              acc[f][ky * 3 + kx] = s;
+            }
+          }
+        }
+        if (S > 0) {
+#pragma unroll
+          for (int p = 0; p < 8; ++p) dbacc += a[p];
+        } else if (j == 0) {
+#pragma unroll
+          for (int p = 0; p < 8; ++p) dbacc += w1[0][1 + p];
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) {
+            w0[f][k] = w1[f][k];
+            w1[f][k] = w2[f][k];
+          }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        float v = acc[f][t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) atomicAdd(&dw[((size_t)j * F + f) * 9 + t], (double)v);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dbacc += __shfl_xor_sync(0xffffffffu, dbacc, o);
+    if (lane == 0 && db != nullptr && (S > 0 || j == 0)) atomicAdd(&db[S > 0 ? j : 0], (double)dbacc);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // elementwise helpers
 // p = sigmoid(logit); a non-finite logit of sample i / per_flag sets
 // nonfinite[i / per_flag]
@@ -335,6 +473,9 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
 // conv_tc.cu's split-bf16 kernel everywhere, 3: same as 0 (kept for A/B
 // scripts)
 extern int g_train_conv_impl;
+// edge weight gradients: 0 = edge_wgrad_kernel (default), 1 = the generic
+// SIMT tile kernel (cross-check)
+int g_edge_wgrad_impl = 0;
 // wgrad_tc.cu: their weight gradient on tcgen05 (split-bf16, `parts` bf16 parts)
 int wgrad_tc32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int parts,
                cudaStream_t st);
@@ -361,6 +502,21 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
 template <int CIN, int COUT>
 static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, double *dw,
                       double *db, cudaStream_t st) {
+  if constexpr ((COUT == 1 && CIN > 2) || (CIN == 2 && COUT > 2)) {
+    // edge convs: the warp-row kernel (one pass over each input)
+    if (g_edge_wgrad_impl == 0) {
+      constexpr int F = COUT == 1 ? 1 : 2;
+      constexpr int S = COUT == 1 ? -1 : 1;
+      const int C = COUT == 1 ? CIN : COUT;
+      const long long tasks = (long long)B * C * ((H + EW_RB - 1) / EW_RB);
+      const int grid = (int)std::min<long long>((tasks + 7) / 8, 148 * 8);
+      const float *many = COUT == 1 ? x : dout, *fewp = COUT == 1 ? dout : x;
+      edge_wgrad_kernel<F, S><<<grid, 256, 0, st>>>(many, fewp, B, C, H, W, dw, db);
+      count_launch();
+      HT_CHECK_LAUNCH();
+      return HT_OK;
+    }
+  }
   if constexpr (CIN == 32 && COUT == 32) {
     // the tensor-core kernel streams rows with TMA (16-B row strides: W % 4 == 0)
     if (g_train_conv_impl != 1 && W % 4 == 0) return wgrad_tc32(x, dout, B, H, W, dw, db, g_wgrad_parts, st);
