@@ -1,4 +1,4 @@
-"""Per-step GPU time of the edge weight-gradient kernels (impl 0 warp-row vs 1
+"""Per-step GPU time of the edge-conv kernels (forward and weight-gradient) (impl 0 warp-row vs 1
 generic tile) inside a config-5-sized backward: 20 x 256^2."""
 import sys, collections, numpy as np, torch
 sys.path.insert(0, '.')
@@ -18,6 +18,6 @@ for impl in (0, 1):
         torch.cuda.synchronize()
     tot = collections.defaultdict(float)
     for e in prof.events():
-        if e.device_type == torch.autograd.DeviceType.CUDA and ('wgrad' in e.name or 'edge' in e.name):
+        if e.device_type == torch.autograd.DeviceType.CUDA and ('wgrad' in e.name or 'edge' in e.name or 'fwd_kernel' in e.name):
             tot[e.name[:60]] += e.time_range.end - e.time_range.start
     print("impl", impl, {k: round(v, 1) for k, v in tot.items() if 'wgt::' not in k})

@@ -147,9 +147,10 @@ int ht_set_train_conv_impl(int impl);
  * reference normwise per tensor, tests/test_gpu_train_cfg5.py) or 3 (six
  * products, fp32 level). */
 int ht_set_wgrad_parts(int parts);
-/* Weight gradients of the edge convs (conv_in 2 -> C, conv_out C -> 1,
- * nn.py:62-77): 0 = warp-per-row kernel reading each input once (default),
- * 1 = the generic SIMT tile kernel (cross-check).  Process-wide. */
+/* Training edge convs (conv_in 2 -> C, conv_out C -> 1; forward, weight
+ * gradients and conv_out's input gradient, nn.py:46-77): 0 = warp-row
+ * kernels reading each input once (default), 1 = the generic SIMT tile
+ * kernels (cross-check).  Process-wide. */
 int ht_set_edge_wgrad_impl(int impl);
 /* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
  * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +

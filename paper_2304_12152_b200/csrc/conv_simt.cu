@@ -327,6 +327,205 @@ __global__ void __launch_bounds__(256) edge_wgrad_kernel(const float *__restrict
   }
 }
 
+// Edge forward convs from few channels to many (conv_in 2 -> C, and the
+// input gradient of conv_out, 1 -> C with the transposed weights;
+// nn.py:46-77): a warp owns RB rows of one image, each lane 8 columns with a
+// 3-row x 10-column register window of the F input channels (each input
+// value read once per task); per output channel the 9 F weights are
+// broadcast from shared memory and the 8 outputs stored as two 16-B stores.
+constexpr int EF_RB = 2;
+template <int F>
+__global__ void __launch_bounds__(256) edge_fwd_f2m_kernel(const float *__restrict__ few, int B, int C, int H, int W,
+                                                           const float *__restrict__ w, const float *__restrict__ bias,
+                                                           float *__restrict__ out, int relu) {
+  __shared__ float ws[32 * F * 9];
+  __shared__ float bs[32];
+  for (int i = threadIdx.x; i < C * F * 9; i += blockDim.x) ws[i] = __ldg(w + i);
+  for (int i = threadIdx.x; i < C; i += blockDim.x) bs[i] = bias ? __ldg(bias + i) : 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long wglob = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
+  const int n_bands = (H + EF_RB - 1) / EF_RB;
+  const long long tasks = (long long)B * n_bands;
+  const size_t plane = (size_t)H * W;
+  const bool vec = (W & 7) == 0;
+  for (long long task = wglob; task < tasks; task += nw) {
+    const int band = (int)(task % n_bands), b = (int)(task / n_bands);
+    const int y0 = band * EF_RB, y1 = min(H, y0 + EF_RB);
+    for (int xc = 0; xc < W; xc += 256) {
+      const int x0 = xc + lane * 8;
+      auto load_row = [&](int yy, float (&dst)[F][10]) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          float cen[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cen[k] = 0.f;
+          float edge = 0.f;
+          if (yy >= 0 && yy < H) {
+            const float *r = few + ((size_t)b * F + f) * plane + (size_t)yy * W;
+            if (vec && x0 + 8 <= W) {
+              const float4 u = __ldg(reinterpret_cast<const float4 *>(r + x0));
+              const float4 v = __ldg(reinterpret_cast<const float4 *>(r + x0 + 4));
+              cen[0] = u.x; cen[1] = u.y; cen[2] = u.z; cen[3] = u.w;
+              cen[4] = v.x; cen[5] = v.y; cen[6] = v.z; cen[7] = v.w;
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (x0 + k < W) cen[k] = __ldg(r + x0 + k);
+            }
+            if (lane == 0 && x0 - 1 >= 0 && x0 - 1 < W) edge = __ldg(r + x0 - 1);
+            if (lane == 31 && x0 + 8 < W) edge = __ldg(r + x0 + 8);
+          }
+          const float left = __shfl_up_sync(0xffffffffu, cen[7], 1);
+          const float right = __shfl_down_sync(0xffffffffu, cen[0], 1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dst[f][1 + k] = cen[k];
+          dst[f][0] = lane > 0 ? left : edge;
+          dst[f][9] = lane < 31 ? right : edge;
+        }
+      };
+      float w0[F][10], w1[F][10], w2[F][10];
+      load_row(y0 - 1, w0);
+      load_row(y0, w1);
+      for (int y = y0; y < y1; ++y) {
+        load_row(y + 1, w2);
+        for (int co = 0; co < C; ++co) {
+          float acc[8];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) acc[p] = bs[co];
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+              const float(&wr)[10] = ky == 0 ? w0[f] : (ky == 1 ? w1[f] : w2[f]);
+#pragma unroll
+              for (int kx = 0; kx < 3; ++kx) {
+                const float wv = ws[((co * F + f) * 3 + ky) * 3 + kx];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) acc[p] = fmaf(wr[p + kx], wv, acc[p]);
+              }
+            }
+          if (relu) {
+#pragma unroll
+            for (int p = 0; p < 8; ++p) acc[p] = fmaxf(acc[p], 0.f);
+          }
+          float *o = out + ((size_t)b * C + co) * plane + (size_t)y * W + x0;
+          if (vec && x0 + 8 <= W) {
+            reinterpret_cast<float4 *>(o)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            reinterpret_cast<float4 *>(o)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          } else {
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+              if (x0 + p < W) o[p] = acc[p];
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) {
+            w0[f][k] = w1[f][k];
+            w1[f][k] = w2[f][k];
+          }
+      }
+    }
+  }
+}
+
+// Edge forward conv from many channels to one (conv_out C -> 1, nn.py:46-60):
+// a CTA owns EM_RB rows of one image; its 8 warps split the input channels
+// (warp k: channels k, k+8, ...), each lane 8 columns and the EM_RB x 8
+// partial sums, a channel's rows held in a register window (each input row
+// read (RB + 2) / RB times); the warps' partials are summed through shared
+// memory in a fixed order (deterministic).
+constexpr int EM_RB = 4;
+__global__ void __launch_bounds__(256, 2) edge_fwd_m2o_kernel(const float *__restrict__ x, int B, int C, int H, int W,
+                                                           const float *__restrict__ w, const float *__restrict__ bias,
+                                                           float *__restrict__ out) {
+  __shared__ float ws[32 * 9];
+  __shared__ float red[8][EM_RB][256];
+  for (int i = threadIdx.x; i < C * 9; i += blockDim.x) ws[i] = __ldg(w + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n_bands = (H + EM_RB - 1) / EM_RB;
+  const long long tasks = (long long)B * n_bands;
+  const size_t plane = (size_t)H * W;
+  const bool vec = (W & 7) == 0;
+  const float b0v = bias ? __ldg(bias) : 0.f;
+  for (long long task = blockIdx.x; task < tasks; task += gridDim.x) {
+    const int band = (int)(task % n_bands), b = (int)(task / n_bands);
+    const int y0 = band * EM_RB;
+    for (int xc = 0; xc < W; xc += 256) {
+      const int x0 = xc + lane * 8;
+      float acc[EM_RB][8];
+#pragma unroll
+      for (int i = 0; i < EM_RB; ++i)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[i][p] = 0.f;
+      for (int ci = warp; ci < C; ci += 8) {
+        const float *xp = x + ((size_t)b * C + ci) * plane;
+        float rows[EM_RB + 2][10];
+#pragma unroll
+        for (int i = 0; i < EM_RB + 2; ++i) {
+          const int yy = y0 - 1 + i;
+          float cen[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cen[k] = 0.f;
+          float edge = 0.f;
+          if (yy >= 0 && yy < H) {
+            const float *r = xp + (size_t)yy * W;
+            if (vec && x0 + 8 <= W) {
+              const float4 u = __ldg(reinterpret_cast<const float4 *>(r + x0));
+              const float4 v = __ldg(reinterpret_cast<const float4 *>(r + x0 + 4));
+              cen[0] = u.x; cen[1] = u.y; cen[2] = u.z; cen[3] = u.w;
+              cen[4] = v.x; cen[5] = v.y; cen[6] = v.z; cen[7] = v.w;
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (x0 + k < W) cen[k] = __ldg(r + x0 + k);
+            }
+            if (lane == 0 && x0 - 1 >= 0 && x0 - 1 < W) edge = __ldg(r + x0 - 1);
+            if (lane == 31 && x0 + 8 < W) edge = __ldg(r + x0 + 8);
+          }
+          const float left = __shfl_up_sync(0xffffffffu, cen[7], 1);
+          const float right = __shfl_down_sync(0xffffffffu, cen[0], 1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) rows[i][1 + k] = cen[k];
+          rows[i][0] = lane > 0 ? left : edge;
+          rows[i][9] = lane < 31 ? right : edge;
+        }
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx) {
+            const float wv = ws[ci * 9 + ky * 3 + kx];
+#pragma unroll
+            for (int i = 0; i < EM_RB; ++i)
+#pragma unroll
+              for (int p = 0; p < 8; ++p) acc[i][p] = fmaf(rows[i + ky][p + kx], wv, acc[i][p]);
+          }
+      }
+      // partials -> shared memory; the sum over warps in warp order
+#pragma unroll
+      for (int i = 0; i < EM_RB; ++i) {
+        float4 *d = reinterpret_cast<float4 *>(&red[warp][i][lane * 8]);
+        d[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        d[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < EM_RB * 256; e += blockDim.x) {
+        const int i = e / 256, col = e % 256, y = y0 + i, xx = xc + col;
+        if (y < H && xx < W) {
+          float v = b0v;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v += red[k][i][col];
+          out[(size_t)b * plane + (size_t)y * W + xx] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // elementwise helpers
 // p = sigmoid(logit); a non-finite logit of sample i / per_flag sets
@@ -485,6 +684,28 @@ template <int CIN, int COUT>
 static int conv_fwd(const float *x, int B, int H, int W, const float *w, const float *bias,
                     const float *mask, const float *resid, float *out, int relu,
                     cudaStream_t st) {
+  if constexpr (COUT == 1 && CIN > 2 && CIN <= 32) {
+    // edge conv many -> one (conv_out)
+    if (g_edge_wgrad_impl == 0 && !mask && !resid && !relu) {
+      const long long tasks = (long long)B * ((H + EM_RB - 1) / EM_RB);
+      const int grid = (int)std::min<long long>(tasks, 148 * 8);
+      edge_fwd_m2o_kernel<<<grid, 256, 0, st>>>(x, B, CIN, H, W, w, bias, out);
+      count_launch();
+      HT_CHECK_LAUNCH();
+      return HT_OK;
+    }
+  }
+  if constexpr (CIN <= 2 && COUT > 2 && COUT <= 32) {
+    // edge convs few -> many (conv_in, conv_out's input gradient)
+    if (g_edge_wgrad_impl == 0 && !mask && !resid) {
+      const long long tasks = (long long)B * ((H + EF_RB - 1) / EF_RB);
+      const int grid = (int)std::min<long long>((tasks + 7) / 8, 148 * 16);
+      edge_fwd_f2m_kernel<CIN><<<grid, 256, 0, st>>>(x, B, COUT, H, W, w, bias, out, relu);
+      count_launch();
+      HT_CHECK_LAUNCH();
+      return HT_OK;
+    }
+  }
   if constexpr (CIN == 32 && COUT == 32) {
     // conv_tc2 (20 x 256^2: 110 vs 134 us plain, 143 vs 162 us with a mask
     // or residual input) wherever the shape allows TMA staging

@@ -103,10 +103,11 @@ def test_tensor_core_forward_matches_oracle():
 
 @pytest.mark.parametrize("C,NB", [(32, 2), (8, 2)])
 @pytest.mark.parametrize("B,H,W", [(2, 37, 61), (3, 40, 256), (1, 70, 264), (2, 33, 300)])
-def test_edge_weight_gradients_warp_row_kernel(C, NB, B, H, W):
-    """conv_in / conv_out weight and bias gradients from the warp-row edge
-    kernel (default) equal the generic SIMT tile kernel's (fp32 sums in a
-    different order: 1e-5 relative per tensor), on aligned and ragged widths."""
+def test_edge_convs_warp_row_kernels(C, NB, B, H, W):
+    """The warp-row edge kernels (default: conv_in's forward and weight
+    gradient, conv_out's weight and input gradients) against the generic SIMT
+    tile kernels (ht_set_edge_wgrad_impl(1)): p and every gradient tensor
+    agree to fp32 summation-order level, on aligned and ragged widths."""
     import torch
     from paper_2304_12152_b200 import _lib
     from paper_2304_12152_b200.nn import PolicyNetwork
@@ -115,24 +116,20 @@ def test_edge_weight_gradients_warp_row_kernel(C, NB, B, H, W):
     r = Rng(6)
     x = np.stack((r.uniforms(B * H * W).reshape(B, H, W), r.gaussians(B * H * W).reshape(B, H, W)), axis=1)
     dp = r.gaussians(B * H * W).reshape(B, H, W) * 1e-3
-    grads = []
+    grads, ps = [], []
     for impl in (0, 1):
         _lib.call("ht_set_edge_wgrad_impl", impl)
         try:
             xd = torch.from_numpy(x.astype(np.float32)).cuda()
-            net.forward_device(xd)
+            ps.append(net.forward_device(xd).double().cpu().numpy())
             g = torch.zeros(net.num_params(), dtype=torch.float64, device="cuda")
             net.backward_device(torch.from_numpy(dp.astype(np.float32)).cuda(), g)
             grads.append(g.cpu().numpy())
         finally:
             _lib.call("ht_set_edge_wgrad_impl", 0)
+    assert np.max(np.abs(ps[0] - ps[1])) <= 1e-6
     sizes = [p.value.size for p in net.params()]
     offs = np.cumsum([0] + sizes)
-    # conv_in.w, conv_in.b, conv_out.w, conv_out.b: the first two and last two tensors
-    for k in (0, 1, len(sizes) - 2, len(sizes) - 1):
+    for k in range(len(sizes)):
         a, b = grads[0][offs[k]:offs[k + 1]], grads[1][offs[k]:offs[k + 1]]
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
-    # every other tensor is untouched by the switch (up to the order in which
-    # the tensor-core weight gradient's CTAs add their fp32 partial sums)
-    mid = slice(offs[2], offs[len(sizes) - 2])
-    assert np.linalg.norm(grads[0][mid] - grads[1][mid]) <= 1e-6 * np.linalg.norm(grads[1][mid])
