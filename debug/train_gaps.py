@@ -9,6 +9,8 @@ from torch.profiler import profile, ProfilerActivity
 cfg = rl.TrainConfig(iterations=1000, batch_size=16, crop_size=256, anisotropy_batch_size=4, hvs_model="gaussian")
 ds = [synth.contone(384, 384, seed=100 + i).astype(np.float64) for i in range(8)]
 rng = Rng(0); net = PolicyNetwork(32, 16); net.init_params(rng); adam = Adam(net.params())
+import gc, os
+if os.environ.get("NOGC"): gc.disable()
 for t in range(4): rl.train_step(net, adam, ds, cfg, rng, t)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
