@@ -9,6 +9,8 @@ H = W = 256
 x = torch.randn(B, 32, H, W, device='cuda'); w = torch.randn(32, 32, 3, 3, device='cuda') * 0.05
 bias = torch.randn(32, device='cuda'); resid = torch.randn_like(x); out = torch.empty_like(x)
 lib = _lib.load()
+import os
+if os.environ.get("PAIR"): _lib.call("ht_set_conv_pair", 1)
 buf = np.zeros((3, 1024, 6), np.int64)
 for it in range(3):
     _lib.call("ht_conv3x3_32", C.c_void_p(x.data_ptr()), B, H, W, C.c_void_p(w.data_ptr()), C.c_void_p(bias.data_ptr()),

@@ -152,6 +152,10 @@ int ht_set_wgrad_parts(int parts);
  * kernels reading each input once (default), 1 = the generic SIMT tile
  * kernels (cross-check).  Process-wide. */
 int ht_set_edge_wgrad_impl(int impl);
+/* The training conv v2 (conv_tc2.cu) on CTA pairs: tcgen05.mma.cta_group::2
+ * (M = 256, each CTA holding half of every weight window) -- 1 = on,
+ * 0 = one CTA per strip.  Process-wide. */
+int ht_set_conv_pair(int on);
 /* One 32 -> 32 training convolution (x, out, mask, resid (B,32,H,W) fp32, w
  * OIHW (32,32,3,3) fp32; bias / mask / resid may be NULL): out = conv(x) +
  * bias, zeroed where mask <= 0, + resid, ReLU if relu -- Conv2d.forward

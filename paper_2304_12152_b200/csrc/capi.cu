@@ -116,6 +116,7 @@ void timing_mark_end(cudaStream_t st) {
 int g_train_conv_impl = 0;
 int g_wgrad_parts = 2;
 extern int g_edge_wgrad_impl;
+extern int g_conv_tc2_pair;
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
 static inline uint64_t splitmix64(uint64_t &s) {
@@ -194,6 +195,13 @@ int ht_timing_read(int *tags, float *ms, int max, int *count) {
 int ht_set_train_conv_impl(int impl) {
   if (impl < 0 || impl > 3) return ht::fail(HT_E_INVALID, "impl must be 0 (tensor core), 1 (simt), 2 (split bf16) or 3 (fp16 pairs)");
   ht::g_train_conv_impl = impl;
+  return HT_OK;
+}
+
+// Training conv v2 on CTA pairs (cta_group::2): 0 = off (default), 1 = on.
+int ht_set_conv_pair(int on) {
+  if (on != 0 && on != 1) return ht::fail(HT_E_INVALID, "on must be 0 or 1");
+  ht::g_conv_tc2_pair = on;
   return HT_OK;
 }
 

@@ -48,13 +48,22 @@ constexpr int NSL = 5;                    // doubled ky sequence [2,1,0,2,1]
 constexpr int NPART = 2;                  // fp16 parts
 constexpr int PLANE = M * 16;             // 8 channels x 128 lanes (fp16)
 constexpr int ROW = 4 * PLANE;            // 32 channels of a row, one part
-constexpr int TILE = 2 * NSL * C * 16;    // B tile (kx, K-half): 160 rows x 2 K-chunks x 16 B
-constexpr int W_BYTES = NPART * 6 * TILE;
-constexpr int A_OFF = W_BYTES;
+// B tile (kx, K-half): WROWS rows x 2 K-chunks x 16 B.  One CTA holds all
+// 160 rows of the doubled ky sequence; a CTA pair (cta_group::2, M = 256)
+// splits every N = 96 window between its CTAs (rows [0, 48) of the window
+// in CTA 0, [48, 96) in CTA 1, at the same address), so each holds 112.
+template <bool PAIR>
+struct WLay {
+  static constexpr int WROWS = PAIR ? 112 : NSL * C;
+  static constexpr int TILE = 2 * WROWS * 16;
+  static constexpr int KSTRIDE = WROWS * 16;          // B K-chunk stride (LBO)
+  static constexpr int W_BYTES = NPART * 6 * TILE;
+};
 constexpr int BOXW = M + 4;               // box: 132 px x 32 channels fp32, [ch][px]
 constexpr int BOX = BOXW * C * 4;
 constexpr int STG_SLOT = 2 * BOX;         // a strip row spans at most two images
-constexpr int NRING = 4;                  // TMEM rings of 96 columns (five measured no faster)
+constexpr int NRING1 = 4;                 // TMEM rings of 96 columns, one CTA per strip (five measured no faster)
+constexpr int NRING2 = 5;                 // CTA pairs: one more row of slack for the cross-CTA ring release
 // barriers (8 B each): acc_full[8], ready[8], ring_free[NRING], stg_full[<=3],
 // stg_empty[<=3], epi_full[2], epi_empty[2].  acc_full / ready are indexed by
 // row & 7 so that no waiter is ever two phases behind its barrier: the two
@@ -65,13 +74,14 @@ constexpr int B_ACC = 0, B_RDY = 8, B_FREE = 16, B_STG = 21, B_STE = 24, B_EF = 
 // Shared-memory layout.  Without an epilogue input: three A buffers and
 // three staging slots (TMA three rows ahead); with one, its rows take two
 // staging slots of their own and the others drop to two each (227 KB).
-template <bool EPI>
+template <bool EPI, bool PAIR>
 struct Lay2 {
+  static constexpr int A_OFF = WLay<PAIR>::W_BYTES;
   static constexpr int NAB = EPI ? 2 : 3;     // A buffers
   static constexpr int NSTG = EPI ? 2 : 3;    // input-row staging slots
   static constexpr int NESTG = EPI ? 2 : 0;   // epilogue-input (mask / residual) row slots
   static constexpr int A_BYTES = NAB * NPART * ROW;
-  static constexpr int STG_OFF = A_OFF + A_BYTES;
+  static constexpr int STG_OFF = A_OFF + A_BYTES;   // (W_BYTES is a multiple of 1 KB)
   static constexpr int ESTG_OFF = STG_OFF + NSTG * STG_SLOT;
   static constexpr int BAR_OFF = ESTG_OFF + NESTG * STG_SLOT;
   static constexpr int MISC_OFF = BAR_OFF + NBARS * 8;   // tmem slot, pad, sx[8], red[2][8], wred[24]
@@ -86,6 +96,7 @@ constexpr int NTHR = NSPL + NDRN + 32 * NISS + 64;   // + issuers + two TMA prod
 constexpr int HC = C / 2;
 constexpr int SCALE_TOP = 14;             // scaled max |x| in [2^(SCALE_TOP-1), 2^SCALE_TOP)
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+constexpr uint32_t IDESC2 = (1u << 4) | ((uint32_t)(96 >> 3) << 17) | ((uint32_t)((2 * M) >> 4) << 24);
 __constant__ int c_ky2[NSL] = {2, 1, 0, 2, 1};
 
 __device__ __forceinline__ float exp2i(int e) { return __int_as_float((127 + e) << 23); }
@@ -102,6 +113,46 @@ __device__ __forceinline__ void split2h(float a, float b, uint32_t &p0, uint32_t
   const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
   p0 = *reinterpret_cast<const uint32_t *>(&h);
   p1 = *reinterpret_cast<const uint32_t *>(&l);
+}
+// cta_group::2: M = 256 over the CTA pair (issued by CTA 0; A and B halves
+// read from the same shared-memory offsets of both CTAs, D in both TMEMs)
+__device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_cta(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"
+      "@P1 bra DONEC_%=;\n\t"
+      "bra WAITC_%=;\n"
+      "DONEC_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -150,7 +201,7 @@ struct Conv2Params {
   float *out;
   int B, H, W, VW, relu;
   int n_strips;
-  long long chunk;    // strip-rows per CTA (strip-major)
+  long long chunk;    // strip-rows per CTA (strip-major; per CTA pair: strip-pair rows)
 };
 
 // the strip-major (strip, row) range [q0, q1) of a CTA, walked as segments
@@ -167,12 +218,19 @@ __device__ __forceinline__ long long next_seg(long long qq, long long q1, int H,
   return end;
 }
 
-template <bool EPI>
+template <bool EPI, bool PAIR>
 __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant__ Conv2Params P) {
-  using L = Lay2<EPI>;
+  using L = Lay2<EPI, PAIR>;
+  using WL = WLay<PAIR>;
   constexpr int NAB = L::NAB, NSTG = L::NSTG, NESTG = EPI ? L::NESTG : 1;
   constexpr int A_BYTES = L::A_BYTES, STG_OFF = L::STG_OFF, ESTG_OFF = L::ESTG_OFF;
-  constexpr int BAR_OFF = L::BAR_OFF, MISC_OFF = L::MISC_OFF;
+  constexpr int BAR_OFF = L::BAR_OFF, MISC_OFF = L::MISC_OFF, A_OFF = L::A_OFF;
+  constexpr int TILE = WL::TILE;
+  // PAIR: CTA `rank` of the pair owns strip 2 u + rank of strip pair u; CTA 0
+  // issues the pair's MMAs, both CTAs' splitters / drainers arrive on CTA 0's
+  // ready / ring_free barriers
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  constexpr int NRING = PAIR ? NRING2 : NRING1;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -195,9 +253,12 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   if (tid == 0) {
     for (int k = 0; k < NSEQ; ++k) {
       mbar_init(bar(B_ACC + k), 1);
-      mbar_init(bar(B_RDY + k), NSPL / 32);
+      // PAIR: CTA 1's splitters / drainers arrive locally and one forwarder
+      // warp passes each completed phase on to CTA 0 (a cluster-scope
+      // release in every splitter / drainer warp cost ~1,300 cycles each)
+      mbar_init(bar(B_RDY + k), NSPL / 32 + (PAIR && rank == 0 ? 1 : 0));
     }
-    for (int k = 0; k < NRING; ++k) mbar_init(bar(B_FREE + k), NDRN / 32);
+    for (int k = 0; k < NRING; ++k) mbar_init(bar(B_FREE + k), NDRN / 32 + (PAIR && rank == 0 ? 1 : 0));
     for (int k = 0; k < NSTG; ++k) {
       mbar_init(bar(B_STG + k), 1);
       mbar_init(bar(B_STE + k), NSPL / 32);
@@ -228,11 +289,13 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     const int ep = i & 3, co = (i >> 2) % C, s = (i >> 2) / C % NSL;
     const int kc = (i >> 2) / C / NSL % 2, kh = (i >> 2) / C / NSL / 2 % 2, kx = (i >> 2) / C / NSL / 4;
     const int ci = kh * 16 + kc * 8 + 2 * ep, ky = c_ky2[s];
+    const int wrow = s * C + co - (PAIR ? 48 * (int)rank : 0);   // row of this CTA's tile
+    if (wrow < 0 || wrow >= WL::WROWS) continue;
     const float wa = __ldg(P.w + ((co * C + ci) * 3 + ky) * 3 + kx) * wsc;
     const float wb = __ldg(P.w + ((co * C + ci + 1) * 3 + ky) * 3 + kx) * wsc;
     uint32_t p0, p1;
     split2h(wa, wb, p0, p1);
-    const int off = (kx * 2 + kh) * TILE + kc * (NSL * C * 16) + (s * C + co) * 16 + ep * 4;
+    const int off = (kx * 2 + kh) * TILE + kc * WL::KSTRIDE + wrow * 16 + ep * 4;
     *reinterpret_cast<uint32_t *>(smem + off) = p0;
     *reinterpret_cast<uint32_t *>(smem + 6 * TILE + off) = p1;
   }
@@ -241,16 +304,34 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   if (tid < C) bias_s[tid] = P.bias ? __ldg(P.bias + tid) : 0.f;
   fence_proxy_async();
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) {
+    // both CTAs' barriers initialised and weights written before any remote
+    // arrive or pair MMA
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const size_t plane = (size_t)P.H * P.W;
-  const long long q0 = (long long)blockIdx.x * P.chunk;
-  const long long q1 = min(q0 + P.chunk, (long long)P.n_strips * P.H);
+  // PAIR: the q space is (strip pair, row), one range per CTA pair
+  const long long n_units = PAIR ? (P.n_strips + 1) / 2 : P.n_strips;
+  const long long q0 = (long long)(PAIR ? blockIdx.x / 2 : blockIdx.x) * P.chunk;
+  const long long q1 = min(q0 + P.chunk, n_units * P.H);
+  // this CTA's strip of segment unit u; a pair's second strip past the last
+  // one stays in the loops (zero inputs, no stores) with its TMA boxes
+  // pointed inside the tensor
+  auto strip_of = [&](int u) { return PAIR ? 2 * u + (int)rank : u; };
+  auto box_image = [&](int v0) { return min(max(v0, 0) / (P.W + 1), P.B - 1); };
   const int WP = P.W + 1;
 
   if (warp == (NSPL + NDRN) / 32 + NISS + 1) {
@@ -260,9 +341,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       for (long long qq = q0; qq < q1;) {
         Seg sg;
         qq = next_seg(qq, q1, P.H, sg);
-        const int v0 = sg.s * S - 1, b0 = max(v0, 0) / WP;
-        const int nbox = (b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
-        const int c0a = (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
+        sg.s = strip_of(sg.s);
+        const bool empty = sg.s >= P.n_strips;   // (PAIR: a pair's missing second strip)
+        const int v0 = sg.s * S - 1, b0 = empty ? 0 : box_image(v0);
+        const int nbox = (!empty && b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
+        const int c0a = empty ? 0 : (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
         for (int d = sg.R0; d < sg.R1; ++d, ++ge) {
           if (ge >= NESTG) mbar_wait(epi_empty(ge), (uint32_t)((ge / NESTG) - 1) & 1u);
           const uint32_t fb = epi_full(ge), dst = sbase + ESTG_OFF + (uint32_t)(ge % NESTG) * STG_SLOT;
@@ -279,9 +362,11 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       for (long long qq = q0; qq < q1;) {
         Seg sg;
         qq = next_seg(qq, q1, P.H, sg);
-        const int v0 = sg.s * S - 1, b0 = max(v0, 0) / WP;
-        const int nbox = (b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
-        const int c0a = (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
+        sg.s = strip_of(sg.s);
+        const bool empty = sg.s >= P.n_strips;   // (PAIR: a pair's missing second strip)
+        const int v0 = sg.s * S - 1, b0 = empty ? 0 : box_image(v0);
+        const int nbox = (!empty && b0 + 1 < P.B && v0 + M - 1 >= (b0 + 1) * WP) ? 2 : 1;
+        const int c0a = empty ? 0 : (v0 - b0 * WP) & ~3, c0b = (v0 - (b0 + 1) * WP) & ~3;
         for (int x = sg.A; x < sg.Bn; ++x, ++tg) {
           // slot tg % NSTG was read by the splitters of row tg - NSTG
           if (tg >= NSTG) mbar_wait(stg_empty(tg), (uint32_t)((tg / NSTG) - 1) & 1u);
@@ -297,30 +382,62 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       }
     }
   } else if (warp >= (NSPL + NDRN) / 32) {
+    if (PAIR && rank != 0) {
+      // CTA 1: the pair's MMAs are issued by CTA 0; warp iss forwards this
+      // CTA's ready (iss 0) / ring_free (iss 1) phases to CTA 0, row by row
+      const int iss = warp - (NSPL + NDRN) / 32;
+      long long n_rows = 0;
+      for (long long qq = q0; qq < q1;) {
+        Seg sg;
+        qq = next_seg(qq, q1, P.H, sg);
+        n_rows += sg.Bn - sg.A;
+      }
+      if (lane == 0) {
+        for (long long g = 0; g < n_rows; ++g) {
+          if (iss == 0) {
+            mbar_wait(ready(g), seq_par(g));
+            mbar_arrive_cluster(map_cta(ready(g), 0));
+          } else {
+            mbar_wait(ring_free(g), (uint32_t)(g / NRING) & 1u);
+            tc_fence_after();
+            tc_fence_before();
+            mbar_arrive_cluster(map_cta(ring_free(g), 0));
+          }
+        }
+      }
+      __syncwarp();
+    } else {
     // ================= issuers: 18 MMAs per row, rows alternating between two
     // warps: while one warp's issue blocks on the tensor pipe's queue, the
     // other waits for its next row's inputs and ring, so the pipe is fed with
     // no gap between batches
     const int iss = warp - (NSPL + NDRN) / 32;
     const uint64_t adesc0 = umma_desc(sbase, PLANE, 128);
-    const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)((NSL * C * 16) >> 4) << 16);
+    const uint64_t bdesc0 = (adesc0 & ~(0x3FFFull << 16)) | ((uint64_t)(WL::KSTRIDE >> 4) << 16);
     long long g = 0;
     for (long long qq = q0; qq < q1;) {
       Seg sg;
       qq = next_seg(qq, q1, P.H, sg);
+        sg.s = strip_of(sg.s);
       int xm3 = sg.A % 3;
       for (int x = sg.A; x < sg.Bn; ++x, ++g, xm3 = xm3 == 2 ? 0 : xm3 + 1) {
         if ((int)(g % NISS) != iss) continue;
         TL2(0, g, 0);
 #ifndef KO_NOWAIT
-        if (lane == 0) mbar_wait(ready(g), seq_par(g));
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_wait_cluster(ready(g), seq_par(g));
+          else mbar_wait(ready(g), seq_par(g));
+        }
 #endif
         __syncwarp();
         TL2(0, g, 1);
         TL2(0, g, 2);
         if (g >= NRING) {
 #ifndef KO_NOWAIT
-          if (lane == 0) mbar_wait(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_wait_cluster(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
+            else mbar_wait(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
+          }
 #endif
           __syncwarp();
         }
@@ -340,19 +457,29 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
 #pragma unroll
             for (int kh = 0; kh < 2; ++kh) {
               const uint64_t a = a0 + kh * KH + kx - 1, b = b0 + (kx * 2 + kh) * TB;
-              mma_f16(d, a + AP, b, acc);
+              if constexpr (PAIR) {
+                mma_f16_pair(d, a + AP, b, acc);
+                mma_f16_pair(d, a, b + BP, 1);
+              } else {
+                mma_f16(d, a + AP, b, acc);
+                mma_f16(d, a, b + BP, 1);
+              }
               acc = 1;
-              mma_f16(d, a, b + BP, 1);
             }
 #pragma unroll
           for (int kx = 0; kx < 3; ++kx)
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) mma_f16(d, a0 + kh * KH + kx - 1, b0 + (kx * 2 + kh) * TB, 1);
-          tc_commit(acc_full(g));
+            for (int kh = 0; kh < 2; ++kh) {
+              if constexpr (PAIR) mma_f16_pair(d, a0 + kh * KH + kx - 1, b0 + (kx * 2 + kh) * TB, 1);
+              else mma_f16(d, a0 + kh * KH + kx - 1, b0 + (kx * 2 + kh) * TB, 1);
+            }
+          if constexpr (PAIR) commit_pair(acc_full(g));
+          else tc_commit(acc_full(g));
         }
         __syncwarp();
         TL2(0, g, 4);
       }
+    }
     }
   } else if (warp < NSPL / 32) {
     // ================= splitters: staged row -> scaled fp16 pair planes =====
@@ -361,6 +488,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     for (long long qq = q0; qq < q1;) {
       Seg sg;
       qq = next_seg(qq, q1, P.H, sg);
+        sg.s = strip_of(sg.s);
       const int v0 = sg.s * S - 1, v = v0 + l;
       const int b = v >= 0 ? v / WP : 0, col = v >= 0 ? v % WP : 0;
       const bool in_img = v >= 0 && v < P.VW && col < P.W;
@@ -445,6 +573,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     for (long long qq = q0; qq < q1;) {
       Seg sg;
       qq = next_seg(qq, q1, P.H, sg);
+        sg.s = strip_of(sg.s);
       const int v = sg.s * S - 1 + l;
       const int b = v >= 0 ? v / WP : 0, col = v >= 0 ? v % WP : 0;
       const bool in_img = v >= 0 && v < P.VW && col < P.W;
@@ -554,10 +683,17 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) {
+    // the pair's last MMAs wrote both TMEMs: no CTA frees its TMEM (or exits,
+    // releasing shared memory the peer's MMAs read) before both are done
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -572,13 +708,19 @@ extern "C" int ht_debug_conv2_timeline(long long *host) {
 // row spans at most two images)
 bool conv_tc2_eligible(int W) { return W % 4 == 0 && W + 1 >= tct2::M; }
 
+// 0: one CTA per strip (cta_group::1), 1: CTA pairs (cta_group::2, M = 256)
+int g_conv_tc2_pair = 0;
+
 int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
                 const float *resid, float *out, int relu, cudaStream_t st) {
   using namespace tct2;
   HT_REQUIRE(conv_tc2_eligible(W), "conv_tc2: unsupported width %d", W);
   HT_REQUIRE(!(mask && resid), "conv_tc2: a ReLU mask and a residual in one launch");
-  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<false>, Lay2<false>::SMEM)) return rc;
-  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<true>, Lay2<true>::SMEM)) return rc;
+  const bool pair = g_conv_tc2_pair != 0;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<false, false>, Lay2<false, false>::SMEM)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<true, false>, Lay2<true, false>::SMEM)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<false, true>, Lay2<false, true>::SMEM)) return rc;
+  if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<true, true>, Lay2<true, true>::SMEM)) return rc;
   int dev = 0, n_sm = 148;
   HT_CUDA(cudaGetDevice(&dev));
   HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
@@ -586,8 +728,10 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
   p.w = w; p.bias = bias; p.mask = mask; p.resid = resid; p.out = out;
   p.B = B; p.H = H; p.W = W; p.VW = B * (W + 1); p.relu = relu;
   p.n_strips = (p.VW + S - 1) / S;
-  const long long total = (long long)p.n_strips * H;
-  long long grid = n_sm;
+  // work units: (strip, row), or (strip pair, row) for CTA pairs
+  const long long units = pair ? (p.n_strips + 1) / 2 : p.n_strips;
+  const long long total = units * H;
+  long long grid = pair ? n_sm / 2 : n_sm;
   if (total < grid * 8) grid = (total + 7) / 8;
   if (grid < 1) grid = 1;
   p.chunk = (total + grid - 1) / grid;
@@ -612,8 +756,25 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     HT_REQUIRE(re == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)re);
   }
-  if (epi) conv_tc2_kernel<true><<<(unsigned)grid, NTHR, Lay2<true>::SMEM, st>>>(p);
-  else conv_tc2_kernel<false><<<(unsigned)grid, NTHR, Lay2<false>::SMEM, st>>>(p);
+  if (!pair) {
+    if (epi) conv_tc2_kernel<true, false><<<(unsigned)grid, NTHR, Lay2<true, false>::SMEM, st>>>(p);
+    else conv_tc2_kernel<false, false><<<(unsigned)grid, NTHR, Lay2<false, false>::SMEM, st>>>(p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * grid), 1, 1);
+    cfg.blockDim = dim3(NTHR, 1, 1);
+    cfg.dynamicSmemBytes = epi ? Lay2<true, true>::SMEM : Lay2<false, true>::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (epi) HT_CUDA(cudaLaunchKernelEx(&cfg, conv_tc2_kernel<true, true>, p));
+    else HT_CUDA(cudaLaunchKernelEx(&cfg, conv_tc2_kernel<false, true>, p));
+  }
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;

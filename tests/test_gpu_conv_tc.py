@@ -93,3 +93,29 @@ def test_conv_tc2_row_scales(xscale, wscale):
     err = np.abs(tc - ref).max(axis=(1, 3))
     assert np.all(np.isfinite(tc))
     assert np.all(err <= bound), float((err / bound).max())
+
+
+@pytest.mark.parametrize("B,H,W", [(3, 9, 128), (5, 2, 252), (1, 7, 300), (2, 11, 256)])
+@pytest.mark.parametrize("mode", ["plain", "mask", "resid"])
+def test_conv_tc2_cta_pairs_bitwise(B, H, W, mode):
+    """The fp16-pair conv on CTA pairs (tcgen05.mma.cta_group::2, M = 256,
+    each CTA holding half of every weight window; ht_set_conv_pair(1)) gives
+    bitwise the one-CTA-per-strip results, odd strip counts included."""
+    from paper_2304_12152_b200 import _lib
+    r = Rng(B * 7 + H * 3 + W)
+    x = r.gaussians(B * 32 * H * W).reshape(B, 32, H, W).astype(np.float32).astype(np.float64)
+    w = (r.gaussians(32 * 32 * 9).reshape(32, 32, 3, 3) * 0.1).astype(np.float32).astype(np.float64)
+    b = r.gaussians(32).astype(np.float32).astype(np.float64)
+    e = r.gaussians(x.size).reshape(x.shape).astype(np.float32).astype(np.float64)
+    kw = dict(bias=b, relu=1)
+    if mode == "mask":
+        kw["mask"] = e
+    elif mode == "resid":
+        kw["resid"] = e
+    single = _run(3, x, w, **kw)
+    _lib.call("ht_set_conv_pair", 1)
+    try:
+        pair = _run(3, x, w, **kw)
+    finally:
+        _lib.call("ht_set_conv_pair", 0)
+    assert np.array_equal(pair, single)
