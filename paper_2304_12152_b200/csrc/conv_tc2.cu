@@ -371,13 +371,9 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
           // slot tg % NSTG was read by the splitters of row tg - NSTG
           if (tg >= NSTG) mbar_wait(stg_empty(tg), (uint32_t)((tg / NSTG) - 1) & 1u);
           const uint32_t fb = stg_full(tg), dst = sbase + STG_OFF + (uint32_t)(tg % NSTG) * STG_SLOT;
-#ifdef KO_TMA
-          mbar_arrive(fb);
-#else
           mbar_expect_tx(fb, nbox * BOX);
           tma_load_4d(dst, &P.tm_x, c0a, 0, x, b0, fb);
           if (nbox == 2) tma_load_4d(dst + BOX, &P.tm_x, c0b, 0, x, b0 + 1, fb);
-#endif
         }
       }
     }
@@ -423,22 +419,18 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       for (int x = sg.A; x < sg.Bn; ++x, ++g, xm3 = xm3 == 2 ? 0 : xm3 + 1) {
         if ((int)(g % NISS) != iss) continue;
         TL2(0, g, 0);
-#ifndef KO_NOWAIT
         if (lane == 0) {
           if constexpr (PAIR) mbar_wait_cluster(ready(g), seq_par(g));
           else mbar_wait(ready(g), seq_par(g));
         }
-#endif
         __syncwarp();
         TL2(0, g, 1);
         TL2(0, g, 2);
         if (g >= NRING) {
-#ifndef KO_NOWAIT
           if (lane == 0) {
             if constexpr (PAIR) mbar_wait_cluster(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
             else mbar_wait(ring_free(g), (uint32_t)((g / NRING) - 1) & 1u);
           }
-#endif
           __syncwarp();
         }
         TL2(0, g, 3);
@@ -501,14 +493,6 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         if (lane == 0) mbar_wait(stg_full(g), (uint32_t)(g / NSTG) & 1u);
         __syncwarp();
         if (warp == 0) TL2(1, g, 1);
-#ifdef KO_SPLIT
-        if (lane == 0) mbar_arrive(stg_empty(g));
-        if (g >= NAB) { if (lane == 0) mbar_wait(acc_full(g - NAB), seq_par(g - NAB)); __syncwarp(); }
-        if (tid == 0) sx_s[g & 7] = 0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(ready(g));
-        continue;
-#endif
         float xin[C];
         const float *src = reinterpret_cast<const float *>(smem + STG_OFF + (uint32_t)(g % NSTG) * STG_SLOT +
                                                            max(kbox, 0) * BOX) + koff;
@@ -599,9 +583,6 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
           float *dst = P.out + pend;
 #pragma unroll
           for (int i = 0; i < HC; ++i) {
-#ifdef V_NOST
-            if (y[i] == 123.456f)
-#endif
             dst[(size_t)i * plane] = y[i];
           }
           pend = ~(size_t)0;
@@ -634,10 +615,6 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
         __syncwarp();
         if (warp == 4) TL2(2, gx(d), 1);
         tc_fence_after();
-#ifdef KO_DRAIN
-        if (d - 1 >= sg.A) release(d - 1);
-        return;
-#endif
         const int slot = d % 3;
         int sxr[3];
 #pragma unroll
