@@ -9,7 +9,7 @@ from torch.profiler import profile, ProfilerActivity
 net = PolicyNetwork(32, 16); net.init_params(Rng(0))
 x = torch.rand(20, 2, 256, 256, device='cuda'); dp = torch.randn(20, 256, 256, device='cuda') * 1e-4
 for impl in (0, 1):
-    _lib.call("ht_set_edge_wgrad_impl", impl)
+    _lib.call("ht_set_edge_conv_impl", impl)
     for _ in range(2):
         net.forward_device(x); g = torch.zeros(net.num_params(), dtype=torch.float64, device='cuda'); net.backward_device(dp, g)
     torch.cuda.synchronize()

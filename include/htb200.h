@@ -151,7 +151,7 @@ int ht_set_wgrad_parts(int parts);
  * gradients and conv_out's input gradient, nn.py:46-77): 0 = warp-row
  * kernels reading each input once (default), 1 = the generic SIMT tile
  * kernels (cross-check).  Process-wide. */
-int ht_set_edge_wgrad_impl(int impl);
+int ht_set_edge_conv_impl(int impl);
 /* The training conv v2 (conv_tc2.cu) on CTA pairs: tcgen05.mma.cta_group::2
  * (M = 256, each CTA holding half of every weight window) -- 1 = on,
  * 0 = one CTA per strip.  Process-wide. */

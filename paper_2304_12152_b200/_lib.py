@@ -47,7 +47,7 @@ SIGNATURES = {
     "ht_timing_read": [_vp, _vp, _i, _ip],
     "ht_set_train_conv_impl": [_i],
     "ht_set_wgrad_parts": [_i],
-    "ht_set_edge_wgrad_impl": [_i],
+    "ht_set_edge_conv_impl": [_i],
     "ht_set_conv_pair": [_i],
     "ht_wgrad3x3_32": [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _vp],
     "ht_conv3x3_32": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],

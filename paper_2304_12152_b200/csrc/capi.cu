@@ -115,7 +115,7 @@ void timing_mark_end(cudaStream_t st) {
 
 int g_train_conv_impl = 0;
 int g_wgrad_parts = 2;
-extern int g_edge_wgrad_impl;
+extern int g_edge_conv_impl;
 extern int g_conv_tc2_pair;
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
@@ -207,9 +207,9 @@ int ht_set_conv_pair(int on) {
 
 // Edge (conv_in / conv_out) weight gradients: 0 = warp-row kernel
 // (default), 1 = the generic SIMT tile kernel (cross-check).
-int ht_set_edge_wgrad_impl(int impl) {
+int ht_set_edge_conv_impl(int impl) {
   if (impl != 0 && impl != 1) return ht::fail(HT_E_INVALID, "impl must be 0 or 1");
-  ht::g_edge_wgrad_impl = impl;
+  ht::g_edge_conv_impl = impl;
   return HT_OK;
 }
 

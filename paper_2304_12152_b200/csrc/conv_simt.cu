@@ -674,7 +674,7 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
 extern int g_train_conv_impl;
 // edge weight gradients: 0 = edge_wgrad_kernel (default), 1 = the generic
 // SIMT tile kernel (cross-check)
-int g_edge_wgrad_impl = 0;
+int g_edge_conv_impl = 0;
 // wgrad_tc.cu: their weight gradient on tcgen05 (split-bf16, `parts` bf16 parts)
 int wgrad_tc32(const float *x, const float *dout, int B, int H, int W, double *dw, double *db, int parts,
                cudaStream_t st);
@@ -686,7 +686,7 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
                     cudaStream_t st) {
   if constexpr (COUT == 1 && CIN > 2 && CIN <= 32) {
     // edge conv many -> one (conv_out)
-    if (g_edge_wgrad_impl == 0 && !mask && !resid && !relu) {
+    if (g_edge_conv_impl == 0 && !mask && !resid && !relu) {
       const long long tasks = (long long)B * ((H + EM_RB - 1) / EM_RB);
       const int grid = (int)std::min<long long>(tasks, 148 * 8);
       edge_fwd_m2o_kernel<<<grid, 256, 0, st>>>(x, B, CIN, H, W, w, bias, out);
@@ -697,7 +697,7 @@ static int conv_fwd(const float *x, int B, int H, int W, const float *w, const f
   }
   if constexpr (CIN <= 2 && COUT > 2 && COUT <= 32) {
     // edge convs few -> many (conv_in, conv_out's input gradient)
-    if (g_edge_wgrad_impl == 0 && !mask && !resid) {
+    if (g_edge_conv_impl == 0 && !mask && !resid) {
       const long long tasks = (long long)B * ((H + EF_RB - 1) / EF_RB);
       const int grid = (int)std::min<long long>((tasks + 7) / 8, 148 * 16);
       edge_fwd_f2m_kernel<CIN><<<grid, 256, 0, st>>>(x, B, COUT, H, W, w, bias, out, relu);
@@ -725,7 +725,7 @@ static int conv_wgrad(const float *x, const float *dout, int B, int H, int W, do
                       double *db, cudaStream_t st) {
   if constexpr ((COUT == 1 && CIN > 2) || (CIN == 2 && COUT > 2)) {
     // edge convs: the warp-row kernel (one pass over each input)
-    if (g_edge_wgrad_impl == 0) {
+    if (g_edge_conv_impl == 0) {
       constexpr int F = COUT == 1 ? 1 : 2;
       constexpr int S = COUT == 1 ? -1 : 1;
       const int C = COUT == 1 ? CIN : COUT;

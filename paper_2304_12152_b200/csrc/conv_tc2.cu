@@ -195,8 +195,8 @@ __device__ long long g_ctl2[3][1024][6];
 
 struct Conv2Params {
   CUtensorMap tm_x;   // x as (W, C, H, B) fp32, box 132 x 32 x 1 x 1
-  CUtensorMap tm_e;   // the mask or residual, same geometry (when has_epi)
-  int has_epi, is_mask;
+  CUtensorMap tm_e;   // the mask or residual, same geometry (EPI kernels)
+  int is_mask;
   const float *w, *bias, *mask, *resid;
   float *out;
   int B, H, W, VW, relu;
@@ -725,7 +725,6 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   HT_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const float *epi = mask ? mask : resid;
-  p.has_epi = epi != nullptr;
   p.is_mask = mask != nullptr;
   if (epi) {
     const CUresult re = enc(&p.tm_e, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(epi), dims, strides, box,

@@ -106,7 +106,7 @@ def test_tensor_core_forward_matches_oracle():
 def test_edge_convs_warp_row_kernels(C, NB, B, H, W):
     """The warp-row edge kernels (default: conv_in's forward and weight
     gradient, conv_out's weight and input gradients) against the generic SIMT
-    tile kernels (ht_set_edge_wgrad_impl(1)): p and every gradient tensor
+    tile kernels (ht_set_edge_conv_impl(1)): p and every gradient tensor
     agree to fp32 summation-order level, on aligned and ragged widths."""
     import torch
     from paper_2304_12152_b200 import _lib
@@ -118,7 +118,7 @@ def test_edge_convs_warp_row_kernels(C, NB, B, H, W):
     dp = r.gaussians(B * H * W).reshape(B, H, W) * 1e-3
     grads, ps = [], []
     for impl in (0, 1):
-        _lib.call("ht_set_edge_wgrad_impl", impl)
+        _lib.call("ht_set_edge_conv_impl", impl)
         try:
             xd = torch.from_numpy(x.astype(np.float32)).cuda()
             ps.append(net.forward_device(xd).double().cpu().numpy())
@@ -126,7 +126,7 @@ def test_edge_convs_warp_row_kernels(C, NB, B, H, W):
             net.backward_device(torch.from_numpy(dp.astype(np.float32)).cuda(), g)
             grads.append(g.cpu().numpy())
         finally:
-            _lib.call("ht_set_edge_wgrad_impl", 0)
+            _lib.call("ht_set_edge_conv_impl", 0)
     assert np.max(np.abs(ps[0] - ps[1])) <= 1e-6
     sizes = [p.value.size for p in net.params()]
     offs = np.cumsum([0] + sizes)
