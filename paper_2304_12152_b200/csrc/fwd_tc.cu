@@ -255,6 +255,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   constexpr int NT = 128 * G;
   constexpr int NABUF = PL::NAB;
   extern __shared__ __align__(1024) uint8_t smem[];
+  // the next pass may be scheduled now: its CTAs take SMs as ours exit and
+  // run their prologue (weights, barriers, TMEM) before waiting for us
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform
   const uint32_t sbase = smem_u32(smem);
@@ -298,6 +301,9 @@ __global__ void __launch_bounds__(128 * Plan<HI, NBK, HO>::G, 1) tc_pass_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  // programmatic dependent launch: the previous pass (which wrote our input
+  // rows and last read the buffer we write) has completed past this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // Balanced work split: this CTA owns strip-rows [q0, q1) of the strip-major
   // (strip, output row) space; it walks them as one segment per strip touched.
@@ -712,8 +718,11 @@ struct PassDesc {
   int layer0;  // index of first layer (0 = conv_in, 1.. = convs, 2NB+1 = conv_out)
 };
 
+// pdl: launched as a programmatic dependent of the previous pass (its
+// prologue overlaps that pass's tail); not while per-pass timing events are
+// recorded between the launches
 template <bool HI, int NBK, bool HO>
-static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
+static int launch_pass(const TcParams &prm, int grid, cudaStream_t st, bool pdl) {
   using PL = Plan<HI, NBK, HO>;
   static_assert(PL::G <= 4 && PL::G <= STRIP_L, "at most 4 layers per pass (halo <= STRIP_L lanes)");
   static_assert(PL::TCOLS <= 512, "TMEM columns exceeded");
@@ -721,7 +730,21 @@ static int launch_pass(const TcParams &prm, int grid, cudaStream_t st) {
   auto kern = tc_pass_kernel<HI, NBK, HO>;
   if (int rc = ensure_smem_attr((const void *)kern, PL::SMEM)) return rc;
   timing_mark_begin(st, (HI ? 100 : 0) + NBK * 10 + (HO ? 1 : 0));
-  kern<<<grid, 128 * PL::G, PL::SMEM, st>>>(prm);
+  if (pdl && !timing_enabled()) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3(128 * PL::G, 1, 1);
+    cfg.dynamicSmemBytes = PL::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HT_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  } else {
+    kern<<<grid, 128 * PL::G, PL::SMEM, st>>>(prm);
+  }
   timing_mark_end(st);
   count_launch();
   HT_CHECK_LAUNCH();
@@ -793,11 +816,11 @@ int run(const void *tc_w, const float *tc_b, int NB, const float *c, const float
     grid = (total + prm.chunk - 1) / prm.chunk;
     const int g = (int)grid;
     int rc;
-    if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, g, st);
-    else if (pd.hi && pd.nbk == 0 && !pd.ho) rc = launch_pass<true, 0, false>(prm, g, st);
-    else if (!pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<false, 2, false>(prm, g, st);
-    else if (!pd.hi && pd.nbk == 1 && pd.ho) rc = launch_pass<false, 1, true>(prm, g, st);
-    else if (!pd.hi && pd.nbk == 0 && pd.ho) rc = launch_pass<false, 0, true>(prm, g, st);
+    if (pd.hi && pd.nbk == 1 && !pd.ho) rc = launch_pass<true, 1, false>(prm, g, st, pi > 0);
+    else if (pd.hi && pd.nbk == 0 && !pd.ho) rc = launch_pass<true, 0, false>(prm, g, st, pi > 0);
+    else if (!pd.hi && pd.nbk == 2 && !pd.ho) rc = launch_pass<false, 2, false>(prm, g, st, pi > 0);
+    else if (!pd.hi && pd.nbk == 1 && pd.ho) rc = launch_pass<false, 1, true>(prm, g, st, pi > 0);
+    else if (!pd.hi && pd.nbk == 0 && pd.ho) rc = launch_pass<false, 0, true>(prm, g, st, pi > 0);
     else return fail(HT_E_UNSUPPORTED, "no kernel for pass (hi=%d nbk=%d ho=%d)", pd.hi, pd.nbk, pd.ho);
     if (rc) return rc;
     in_x = out_x;
