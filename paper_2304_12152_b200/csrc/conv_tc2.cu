@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   constexpr int NRING = PAIR ? NRING2 : NRING1;
   extern __shared__ __align__(1024) uint8_t smem[];
+  pdl_launch_dependents();
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t sbase = smem_u32(smem);
@@ -322,6 +323,10 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
   }
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  // launched as a programmatic dependent: the prologue above (weights,
+  // barriers, TMEM) overlapped the previous kernel; its outputs (our input,
+  // mask / residual) are complete past this point
+  pdl_wait();
   const size_t plane = (size_t)P.H * P.W;
   // PAIR: the q space is (strip pair, row), one range per CTA pair
   const long long n_units = PAIR ? (P.n_strips + 1) / 2 : P.n_strips;
@@ -733,8 +738,8 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
     HT_REQUIRE(re == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)re);
   }
   if (!pair) {
-    if (epi) conv_tc2_kernel<true, false><<<(unsigned)grid, NTHR, Lay2<true, false>::SMEM, st>>>(p);
-    else conv_tc2_kernel<false, false><<<(unsigned)grid, NTHR, Lay2<false, false>::SMEM, st>>>(p);
+    if (epi) HT_CUDA(launch_pdl(conv_tc2_kernel<true, false>, (unsigned)grid, NTHR, Lay2<true, false>::SMEM, st, p));
+    else HT_CUDA(launch_pdl(conv_tc2_kernel<false, false>, (unsigned)grid, NTHR, Lay2<false, false>::SMEM, st, p));
   } else {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];

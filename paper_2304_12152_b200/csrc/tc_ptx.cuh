@@ -211,5 +211,26 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
 }
 
 
+// Launch as a programmatic dependent of the previous kernel in the stream
+// (cudaLaunchAttributeProgrammaticStreamSerialization): the kernel must run
+// griddepcontrol.wait before touching anything that kernel wrote.
+template <typename Kern, typename Arg>
+static inline cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                                     const Arg &arg) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, arg);
+}
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace tc
 }  // namespace ht

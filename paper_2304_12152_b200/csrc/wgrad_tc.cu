@@ -171,6 +171,7 @@ template <int NP>
 __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid_constant__ WgParams P) {
   using L = Lay<NP>;
   extern __shared__ uint8_t smem_raw[];
+  pdl_launch_dependents();
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   // 1024-B alignment for the swizzled TMA boxes
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  pdl_wait();   // (programmatic dependent launch: x and dout are complete from here)
 
   // tiles interleaved over the CTAs (tile blockIdx.x + i * gridDim.x), x fastest
   const long long stride = gridDim.x;
@@ -442,7 +444,7 @@ static int launch(const float *x, const float *dout, int B, int H, int W, double
   p.tiles_x = (W + WT - 1) / WT;
   p.n_tiles = (long long)B * p.tiles_y * p.tiles_x;
   const long long grid = p.n_tiles < n_sm ? p.n_tiles : n_sm;
-  wgrad_tc_kernel<NP><<<(unsigned)grid, L::NTHR, L::SMEM, st>>>(p);
+  HT_CUDA(launch_pdl(wgrad_tc_kernel<NP>, (unsigned)grid, L::NTHR, L::SMEM, st, p));
   count_launch();
   HT_CHECK_LAUNCH();
   return HT_OK;
