@@ -205,6 +205,10 @@ template <int F, int S>
 __global__ void __launch_bounds__(256) edge_wgrad_kernel(const float *__restrict__ many, const float *__restrict__ few,
                                                          int B, int C, int H, int W, double *__restrict__ dw,
                                                          double *__restrict__ db) {
+  // a programmatic dependent launched next (the training convs) may start its
+  // prologue while this kernel runs; it waits for our completion before
+  // reading what we write
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const long long wglob = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), nw = (long long)gridDim.x * 8;
   const int n_bands = (H + EW_RB - 1) / EW_RB;
@@ -338,6 +342,10 @@ template <int F>
 __global__ void __launch_bounds__(256) edge_fwd_f2m_kernel(const float *__restrict__ few, int B, int C, int H, int W,
                                                            const float *__restrict__ w, const float *__restrict__ bias,
                                                            float *__restrict__ out, int relu) {
+  // a programmatic dependent launched next (the training convs) may start its
+  // prologue while this kernel runs; it waits for our completion before
+  // reading what we write
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ float ws[32 * F * 9];
   __shared__ float bs[32];
   for (int i = threadIdx.x; i < C * F * 9; i += blockDim.x) ws[i] = __ldg(w + i);
@@ -441,6 +449,10 @@ constexpr int EM_RB = 4;
 __global__ void __launch_bounds__(256, 2) edge_fwd_m2o_kernel(const float *__restrict__ x, int B, int C, int H, int W,
                                                            const float *__restrict__ w, const float *__restrict__ bias,
                                                            float *__restrict__ out) {
+  // a programmatic dependent launched next (the training convs) may start its
+  // prologue while this kernel runs; it waits for our completion before
+  // reading what we write
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ float ws[32 * 9];
   __shared__ float red[8][EM_RB][256];
   for (int i = threadIdx.x; i < C * 9; i += blockDim.x) ws[i] = __ldg(w + i);
