@@ -142,11 +142,18 @@ class PageEngine:
         for overlap), out_host (out_rows, W) uint8 CPU tensor; returns a
         ticket for wait().  Inputs must stay unchanged and out_host unread
         until then."""
+        import numpy as np
         import torch
         st, s = self.strip, self._sets[self._next % len(self._sets)]
-        self._next += 1
         if tuple(page.shape) != (self.H, self.W) or tuple(noise.shape) != (self.H, self.W):
             raise ValueError(f"page and noise must be ({self.H}, {self.W})")
+        if not isinstance(out_host, torch.Tensor) or tuple(out_host.shape) != self.out_shape() \
+                or out_host.dtype != torch.uint8 or out_host.device.type != "cpu":
+            raise ValueError(f"out_host must be a CPU uint8 tensor of shape {self.out_shape()}")
+        # numpy inputs work too (pageable: their copies do not overlap)
+        page = torch.from_numpy(np.ascontiguousarray(page, dtype=np.float32)) if isinstance(page, np.ndarray) else page
+        noise = torch.from_numpy(np.ascontiguousarray(noise, dtype=np.float32)) if isinstance(noise, np.ndarray) else noise
+        self._next += 1
         stream = s["stream"]
         stream.wait_stream(torch.cuda.current_stream(self.dev))
         r0, r1 = st.in_row0, st.in_row0 + st.in_rows

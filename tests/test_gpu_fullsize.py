@@ -177,6 +177,14 @@ def test_page_engine_streams_pages(monkeypatch):
         e.wait(e.submit(ph[1], zh[1], o))
         stitched[e.strip.out_row0:e.strip.out_row0 + e.strip.out_rows] = o
     assert torch.equal(stitched, refs[1])
+    monkeypatch.undo()
+    # numpy pages (pageable copies) give the same rows; a wrong output buffer is refused
+    e = parallel.PageEngine(net, H, W, depth=1)
+    o = torch.empty(e.out_shape(), dtype=torch.uint8)
+    e.wait(e.submit(pages[2], noises[2].numpy(), o))
+    assert torch.equal(o, refs[2])
+    with pytest.raises(ValueError):
+        e.submit(pages[2], noises[2].numpy(), torch.empty((3, 3), dtype=torch.uint8))
 
 
 def test_config5_data_parallel_gradient_full_size(monkeypatch):
