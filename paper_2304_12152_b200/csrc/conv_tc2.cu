@@ -19,18 +19,28 @@
 // Structure (one CTA per SM, strips of 128 pixel lanes with 126 output lanes,
 // rows streamed top to bottom, MMA(x) for input row x adding into output rows
 // x+1, x, x-1 of TMEM ring x mod 4 through the doubled-ky B window):
-// * issuer warp: TMA of input row x+3 into a 3-slot staging ring, then the 18
-//   MMAs of row x once the splitters have written it and the drainers have
-//   freed ring x mod 4;
+// * two MMA issuer warps (alternate rows): the 18 MMAs of row x once the
+//   splitters have written it and the drainers have freed ring x mod 4 --
+//   while one warp's issue blocks on the tensor pipe's shallow queue the
+//   other waits for its next row;
+// * TMA producer warps: input rows into a staging ring (3 slots; 2 when the
+//   launch has a mask / residual input, whose rows a second producer stages
+//   in a 2-slot ring of their own, two output rows ahead);
 // * 4 splitter warps (thread = pixel lane, 32 channels): staged row -> row
 //   max (warp reduce + 4-warp barrier) -> scaled fp16 pair planes in one of
-//   three A buffers.  They touch no global memory, so the proxy fence that
-//   publishes the planes to the tensor core waits for nothing else;
+//   the A buffers (3; 2 with an epilogue input).  They touch no global
+//   memory, so the proxy fence that publishes the planes to the tensor core
+//   waits for nothing else;
 // * 8 drainer warps (thread = pixel lane x 16 channels): wait for the MMAs of
-//   an output row's three input rows, unscale and sum the rings, epilogue,
-//   coalesced NCHW stores, and the next row's mask / residual loads.
+//   an output row's three input rows, unscale and sum the rings (one at a
+//   time), release the ring, epilogue with the staged mask / residual,
+//   coalesced NCHW stores deferred past the next row's loads.
 // Splitting, MMAs and draining of different rows overlap: the tensor pipe
-// works on MMA(x) while row x+1 is split and row x-2 is drained.
+// works on MMA(x) while row x+1 is split and row x-2 is drained.  Launched
+// as a programmatic dependent of the previous kernel (the prologue -- weight
+// split, barriers, TMEM -- overlaps its tail; griddepcontrol.wait before the
+// first read of its output).  PAIR (opt-in, ht_set_conv_pair): the same on
+// CTA pairs with tcgen05.mma.cta_group::2 (measured slower, kept tested).
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
