@@ -214,9 +214,9 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
 // Launch as a programmatic dependent of the previous kernel in the stream
 // (cudaLaunchAttributeProgrammaticStreamSerialization): the kernel must run
 // griddepcontrol.wait before touching anything that kernel wrote.
-template <typename Kern, typename Arg>
+template <typename Kern, typename... Args>
 static inline cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                                     const Arg &arg) {
+                                     Args... args) {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -227,7 +227,7 @@ static inline cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, s
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, arg);
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

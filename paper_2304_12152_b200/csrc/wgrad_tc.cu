@@ -381,22 +381,32 @@ __global__ void __launch_bounds__(Lay<NP>::NTHR, 1) wgrad_tc_kernel(const __grid
   __syncthreads();
   tc_fence_after();
   // ---- D2 -> dW (fp64) by the converter warps: TMEM lane = ky' * 32 + ci,
-  //      column = (s, kx, co)
+  //      column = (s, kx, co).  Every dW element has two entries (s = 0, 1;
+  //      ky' = ky + s): D2 goes through shared memory (the operand and raw
+  //      buffers are free now) and each element is added with one fp64
+  //      atomic instead of two (the 148 CTAs' atomics on the same 9216
+  //      addresses are the kernel's tail: ~20 us per launch with two)
   if (n_tiles > 0 && warp < L::MMA_WARP) {
     constexpr int CPW = NCOL / (NCONV / 128);   // columns per warp
-    const int quarter = warp & 3, ci = lane;
+    constexpr int DP2 = NCOL + 1;               // padded row: conflict-free column-wise stores
+    static_assert(128 * DP2 * 4 <= L::BAR_OFF, "D2 staging exceeds the free buffers");
+    float *d2s = reinterpret_cast<float *>(smem);
+    const int quarter = warp & 3;
     const int c_lo = (warp >> 2) * CPW;
 #pragma unroll
     for (int cc = 0; cc < CPW; cc += 16) {
       float v[16];
       tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + D2_COL + c_lo + cc, v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int n = c_lo + cc + i;
-        const int s = n / (3 * C), kx = (n / C) % 3, co = n % C;
-        const int ky = quarter - s;
-        if (ky >= 0 && ky <= 2) atomicAdd(P.dw + ((size_t)(co * C + ci) * 3 + ky) * 3 + kx, (double)v[i]);
-      }
+      for (int i = 0; i < 16; ++i) d2s[(quarter * 32 + lane) * DP2 + c_lo + cc + i] = v[i];
+    }
+    named_bar(1, NCONV);
+    for (int t = tid; t < C * C * 9; t += NCONV) {
+      const int co = t % C, kx = (t / C) % 3, ky = (t / (3 * C)) % 3, ci = t / (9 * C);
+      double sum = 0.0;
+#pragma unroll
+      for (int sp = 0; sp < TY; ++sp) sum += (double)d2s[((ky + sp) * C + ci) * DP2 + (sp * 3 + kx) * C + co];
+      atomicAdd(P.dw + ((size_t)(co * C + ci) * 3 + ky) * 3 + kx, sum);
     }
   }
   if (tid < C && P.db) atomicAdd(P.db + tid, (double)db_s[tid]);
