@@ -152,6 +152,13 @@ int ht_set_wgrad_parts(int parts);
  * kernels reading each input once (default), 1 = the generic SIMT tile
  * kernels (cross-check).  Process-wide. */
 int ht_set_edge_conv_impl(int impl);
+/* Training ReLU bits (the _relu_mask of ResidualBlock, nn.py:89-100): 1 =
+ * on the TMA-staged training-conv path the forward stores each conv1's ReLU
+ * as bits (4 B per pixel) that conv2's input gradient reads instead of the
+ * fp32 activation, and conv1's input gradient is added onto the skip
+ * gradient in place (default); 0 = fp32 mask / residual epilogue inputs
+ * (cross-check).  Process-wide; a backward follows what its forward did. */
+int ht_set_train_bits(int on);
 /* The training conv v2 (conv_tc2.cu) on CTA pairs: tcgen05.mma.cta_group::2
  * (M = 256, each CTA holding half of every weight window) -- 1 = on,
  * 0 = one CTA per strip.  Process-wide. */

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ht_timing_reserve": [_i],
     "ht_timing_read": [_vp, _vp, _i, _ip],
     "ht_set_train_conv_impl": [_i],
+    "ht_set_train_bits": [_i],
     "ht_set_wgrad_parts": [_i],
     "ht_set_edge_conv_impl": [_i],
     "ht_set_conv_pair": [_i],

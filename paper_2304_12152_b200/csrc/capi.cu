@@ -116,6 +116,7 @@ void timing_mark_end(cudaStream_t st) {
 int g_train_conv_impl = 0;
 int g_wgrad_parts = 2;
 extern int g_edge_conv_impl;
+extern int g_train_bits;
 extern int g_conv_tc2_pair;
 
 // ---- xoshiro256++ / splitmix64 (imagecore.py:14-21, 52-64) -------------
@@ -210,6 +211,12 @@ int ht_set_conv_pair(int on) {
 int ht_set_edge_conv_impl(int impl) {
   if (impl != 0 && impl != 1) return ht::fail(HT_E_INVALID, "impl must be 0 or 1");
   ht::g_edge_conv_impl = impl;
+  return HT_OK;
+}
+
+int ht_set_train_bits(int on) {
+  if (on != 0 && on != 1) return ht::fail(HT_E_INVALID, "on must be 0 or 1");
+  ht::g_train_bits = on;
   return HT_OK;
 }
 

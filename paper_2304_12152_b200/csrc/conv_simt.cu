@@ -7,6 +7,8 @@
 // ResidualBlock (nn.py:91-100); PolicyNetwork (nn.py:138-160).  Tensors are
 // NCHW float32; gradients accumulate into a flat float64 vector in
 // params() order.
+#include <mutex>
+#include <set>
 #include <math.h>
 
 #include <vector>
@@ -679,11 +681,35 @@ int conv_tc32(const float *x, int B, int H, int W, const float *w, const float *
 bool conv_tc2_eligible(int W);
 int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
                 const float *resid, float *out, int relu, cudaStream_t st);
+int conv_tc2_32_ex(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+                   const float *resid, float *out, int relu, uint16_t *bits_out, const uint16_t *bits_in,
+                   int accum, cudaStream_t st);
 // 0: tensor cores for 32 -> 32 convs (default: conv_tc2 where the shape
 // allows TMA staging, conv_tc otherwise), 1: SIMT only, 2: tensor cores with
 // conv_tc.cu's split-bf16 kernel everywhere, 3: same as 0 (kept for A/B
 // scripts)
 extern int g_train_conv_impl;
+// 1 (default): on the conv_tc2 path the training forward stores each conv1's
+// ReLU as bits (4 B per pixel) and the backward reads those instead of the
+// fp32 activation, and adds the conv1 input gradient onto the skip gradient
+// in place; 0: fp32 mask / residual epilogue inputs (cross-check)
+int g_train_bits = 1;
+static bool train_bits_path(int C, int W) {
+  return C == 32 && g_train_bits && (g_train_conv_impl == 0 || g_train_conv_impl == 3) && conv_tc2_eligible(W);
+}
+// activation workspaces whose ReLU bits the last forward into them wrote (the
+// backward takes the bits path only for those, whatever the settings now)
+static std::mutex g_bits_mu;
+static std::set<const void *> g_bits_acts;
+static void note_bits(const void *act, bool valid) {
+  std::lock_guard<std::mutex> lk(g_bits_mu);
+  if (valid) g_bits_acts.insert(act);
+  else g_bits_acts.erase(act);
+}
+static bool has_bits(const void *act) {
+  std::lock_guard<std::mutex> lk(g_bits_mu);
+  return g_bits_acts.count(act) != 0;
+}
 // edge weight gradients: 0 = edge_wgrad_kernel (default), 1 = the generic
 // SIMT tile kernel (cross-check)
 int g_edge_conv_impl = 0;
@@ -799,7 +825,8 @@ static PackPtrs pack_ptrs(const void *packed, int C, int NB) {
 // Forward over (B, 2, H, W).  keep != nullptr: training mode, activations
 // stored as y[0..NB] and r[0..NB-1] (each B*C*H*W); else ping-pong scratch.
 static int simt_forward(const void *packed, int C, int NB, const float *x, int B, int H,
-                        int W, float *scratch, bool keep, float *logits, cudaStream_t st) {
+                        int W, float *scratch, bool keep, float *logits, cudaStream_t st,
+                        uint16_t *bits = nullptr) {
   NetGeom g(C, NB);
   PackPtrs P = pack_ptrs(packed, C, NB);
   const size_t act = (size_t)B * C * H * W;
@@ -811,8 +838,12 @@ static int simt_forward(const void *packed, int C, int NB, const float *x, int B
                          ybuf(0), 0, st);
     if (rc) return rc;
     for (int k = 0; k < NB; ++k) {
-      rc = conv_fwd<CC, CC>(ybuf(k), B, H, W, P.f32 + g.w1(k), P.f32 + g.b1(k), nullptr,
-                            nullptr, rbuf(k), 1, st);
+      if (bits)
+        rc = conv_tc2_32_ex(ybuf(k), B, H, W, P.f32 + g.w1(k), P.f32 + g.b1(k), nullptr, nullptr, rbuf(k), 1,
+                            bits + (size_t)k * 2 * B * H * W, nullptr, 0, st);
+      else
+        rc = conv_fwd<CC, CC>(ybuf(k), B, H, W, P.f32 + g.w1(k), P.f32 + g.b1(k), nullptr,
+                              nullptr, rbuf(k), 1, st);
       if (rc) return rc;
       rc = conv_fwd<CC, CC>(rbuf(k), B, H, W, P.f32 + g.w2(k), P.f32 + g.b2(k), nullptr,
                             ybuf(k), ybuf(k + 1), 0, st);
@@ -866,8 +897,10 @@ extern "C" {
 
 int ht_train_act_bytes(int channels, int blocks, int B, int H, int W, int64_t *bytes) {
   const size_t act = (size_t)B * channels * H * W;
-  // y[0..NB], r[0..NB-1], logits, 3 backward temporaries
-  *bytes = (int64_t)sizeof(float) * ((2 * (size_t)blocks + 1) * act + (size_t)B * H * W + 3 * act);
+  // y[0..NB], r[0..NB-1], logits, 3 backward temporaries, then the conv1
+  // ReLU bits (blocks x B x 2 x H x W uint16) of the conv_tc2 path
+  *bytes = (int64_t)sizeof(float) * ((2 * (size_t)blocks + 1) * act + (size_t)B * H * W + 3 * act) +
+           (int64_t)sizeof(uint16_t) * 2 * (size_t)blocks * B * H * W;
   return HT_OK;
 }
 
@@ -883,7 +916,10 @@ int ht_policy_forward_train_async(const void *packed, int C, int NB, const float
   const size_t a = (size_t)B * C * H * W;
   float *scratch = (float *)act;
   float *logits = scratch + (2 * (size_t)NB + 1) * a;
-  int rc = ht::simt_forward(packed, C, NB, x, B, H, W, scratch, true, logits, st);
+  uint16_t *bits = ht::train_bits_path(C, W)
+                       ? reinterpret_cast<uint16_t *>(logits + (size_t)B * H * W + 3 * a) : nullptr;
+  ht::note_bits(act, bits != nullptr);
+  int rc = ht::simt_forward(packed, C, NB, x, B, H, W, scratch, true, logits, st, bits);
   if (rc) return rc;
   // sigmoid + finite check (nn.py:147-149)
   const int64_t n = (int64_t)B * H * W;
@@ -929,6 +965,8 @@ int ht_policy_backward(const void *packed, int C, int NB, const float *x, int B,
   auto r = [&](int k) { return scratch + a * (NB + 1 + k); };
   float *tmp = (float *)(scratch + (2 * (size_t)NB + 1) * a + (size_t)B * H * W);
   float *dy = tmp, *dt = tmp + a, *dy2 = tmp + 2 * a;
+  // the forward stored conv1's ReLU as bits when it took this path
+  const uint16_t *bits = ht::has_bits(act) ? reinterpret_cast<const uint16_t *>(tmp + 3 * a) : nullptr;
   // dlogits into dt's first plane-set (B*H*W floats)
   float *dl = dt;
   const int64_t n = (int64_t)B * H * W;
@@ -946,11 +984,22 @@ int ht_policy_backward(const void *packed, int C, int NB, const float *x, int B,
     for (int k = NB - 1; k >= 0; --k) {
       rc = ht::conv_wgrad<CC, CC>(r(k), dy, B, H, W, grad + g.w2(k), grad + g.b2(k), st);
       if (rc) return rc;
-      rc = ht::conv_fwd<CC, CC>(dy, B, H, W, P.f32t + g.w2(k), nullptr, r(k), nullptr, dt, 0,
-                                st);
+      if (bits)
+        rc = ht::conv_tc2_32_ex(dy, B, H, W, P.f32t + g.w2(k), nullptr, nullptr, nullptr, dt, 0, nullptr,
+                                bits + (size_t)k * 2 * B * H * W, 0, st);
+      else
+        rc = ht::conv_fwd<CC, CC>(dy, B, H, W, P.f32t + g.w2(k), nullptr, r(k), nullptr, dt, 0,
+                                  st);
       if (rc) return rc;
       rc = ht::conv_wgrad<CC, CC>(y(k), dt, B, H, W, grad + g.w1(k), grad + g.b1(k), st);
       if (rc) return rc;
+      if (bits) {
+        // dy += conv1^T(dt), in place (same fp32 sum as the residual epilogue)
+        rc = ht::conv_tc2_32_ex(dt, B, H, W, P.f32t + g.w1(k), nullptr, nullptr, nullptr, dy, 0, nullptr,
+                                nullptr, 1, st);
+        if (rc) return rc;
+        continue;
+      }
       rc = ht::conv_fwd<CC, CC>(dt, B, H, W, P.f32t + g.w1(k), nullptr, nullptr, dy, dy2, 0,
                                 st);
       if (rc) return rc;

@@ -209,6 +209,14 @@ struct Conv2Params {
   int is_mask;
   const float *w, *bias, *mask, *resid;
   float *out;
+  // training-path extras (conv_tc2_32_ex): ReLU bits written by a forward
+  // conv1 / read by the input gradient of conv2 instead of an fp32 mask, one
+  // uint16 per (image, channel half, pixel) = bit i: channel half*16+i > 0;
+  // accum: out += conv (red.global.add) -- the conv1 input gradient adds onto
+  // the skip gradient in place instead of reading it as a residual
+  uint16_t *bits_out;
+  const uint16_t *bits_in;
+  int accum;
   int B, H, W, VW, relu;
   int n_strips;
   long long chunk;    // strip-rows per CTA (strip-major; per CTA pair: strip-pair rows)
@@ -596,15 +604,23 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
       auto flush = [&]() {
         if (pend != ~(size_t)0) {
           float *dst = P.out + pend;
+          if (!EPI && P.accum) {
 #pragma unroll
-          for (int i = 0; i < HC; ++i) {
-            dst[(size_t)i * plane] = y[i];
+            for (int i = 0; i < HC; ++i) red_add_f32(dst + (size_t)i * plane, y[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < HC; ++i) dst[(size_t)i * plane] = y[i];
           }
           pend = ~(size_t)0;
         }
       };
+      // ReLU bits of (image b, this channel half): one uint16 per pixel
+      const size_t bbase = ((size_t)b * 2 + half) * plane + col;
       auto drain_row = [&](int d) {
         float e[HC];
+        uint32_t mb = 0xffffu;
+        // (issued before the completion wait: its latency hides behind it)
+        if (!EPI && P.bits_in && lane_valid) mb = __ldg(P.bits_in + bbase + (size_t)d * P.W);
         if (has_epi) {
           // this row's mask / residual from its staging slot; the slot is
           // released at once (the arrive orders the reads before it)
@@ -661,7 +677,14 @@ __global__ void __launch_bounds__(NTHR, 1) conv_tc2_kernel(const __grid_constant
             if (is_mask) y[i] = e[i] > 0.f ? y[i] : 0.f;
             else y[i] += e[i];
           }
+          if (!EPI) y[i] = (mb >> i) & 1u ? y[i] : 0.f;
           if (P.relu) y[i] = fmaxf(y[i], 0.f);
+        }
+        if (!EPI && P.bits_out && lane_valid) {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int i = 0; i < HC; ++i) bits |= (y[i] > 0.f ? 1u : 0u) << i;
+          P.bits_out[bbase + (size_t)d * P.W] = (uint16_t)bits;
         }
         if (lane_valid) pend = obase + (size_t)d * P.W;
         if (warp == 4) TL2(2, gx(d), 3);
@@ -703,11 +726,22 @@ bool conv_tc2_eligible(int W) { return W % 4 == 0 && W + 1 >= tct2::M; }
 // 0: one CTA per strip (cta_group::1), 1: CTA pairs (cta_group::2, M = 256)
 int g_conv_tc2_pair = 0;
 
+int conv_tc2_32_ex(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+                   const float *resid, float *out, int relu, uint16_t *bits_out, const uint16_t *bits_in,
+                   int accum, cudaStream_t st);
 int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
                 const float *resid, float *out, int relu, cudaStream_t st) {
+  return conv_tc2_32_ex(x, B, H, W, w, bias, mask, resid, out, relu, nullptr, nullptr, 0, st);
+}
+
+int conv_tc2_32_ex(const float *x, int B, int H, int W, const float *w, const float *bias, const float *mask,
+                   const float *resid, float *out, int relu, uint16_t *bits_out, const uint16_t *bits_in,
+                   int accum, cudaStream_t st) {
   using namespace tct2;
   HT_REQUIRE(conv_tc2_eligible(W), "conv_tc2: unsupported width %d", W);
   HT_REQUIRE(!(mask && resid), "conv_tc2: a ReLU mask and a residual in one launch");
+  HT_REQUIRE(!((mask || resid) && (bits_in || bits_out || accum)),
+             "conv_tc2: ReLU bits / accumulation only without an fp32 epilogue input");
   const bool pair = g_conv_tc2_pair != 0;
   if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<false, false>, Lay2<false, false>::SMEM)) return rc;
   if (int rc = ensure_smem_attr((const void *)conv_tc2_kernel<true, false>, Lay2<true, false>::SMEM)) return rc;
@@ -718,6 +752,7 @@ int conv_tc2_32(const float *x, int B, int H, int W, const float *w, const float
   HT_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   Conv2Params p{};
   p.w = w; p.bias = bias; p.mask = mask; p.resid = resid; p.out = out;
+  p.bits_out = bits_out; p.bits_in = bits_in; p.accum = accum;
   p.B = B; p.H = H; p.W = W; p.VW = B * (W + 1); p.relu = relu;
   p.n_strips = (p.VW + S - 1) / S;
   // work units: (strip, row), or (strip pair, row) for CTA pairs

@@ -231,6 +231,10 @@ static inline cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, s
 }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// fire-and-forget fp32 add at L2 (round to nearest; subnormals flushed)
+__device__ __forceinline__ void red_add_f32(float *p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 
 }  // namespace tc
 }  // namespace ht

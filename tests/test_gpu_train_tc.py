@@ -133,3 +133,43 @@ def test_edge_convs_warp_row_kernels(C, NB, B, H, W):
     for k in range(len(sizes)):
         a, b = grads[0][offs[k]:offs[k + 1]], grads[1][offs[k]:offs[k + 1]]
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
+
+
+@pytest.mark.parametrize("B,H,W", [(2, 33, 256), (1, 7, 300), (3, 20, 132)])
+def test_relu_bits_and_in_place_skip_gradient(B, H, W):
+    """Training ReLU bits (default on the TMA-staged path: each conv1's mask
+    stored as 4 B per pixel, conv2's input gradient reads the bits, conv1's
+    input gradient is added onto the skip gradient in place) against the fp32
+    mask / residual epilogue inputs (ht_set_train_bits(0)): p bitwise, dx and
+    every gradient tensor to fp32 summation-order level.  A backward follows
+    its forward's setting even when the setting changes in between."""
+    import torch
+    from paper_2304_12152_b200 import _lib
+    from paper_2304_12152_b200.nn import PolicyNetwork
+    net = PolicyNetwork(32, 3)
+    net.init_params(Rng(8), std=0.05)
+    r = Rng(9)
+    x = np.stack((r.uniforms(B * H * W).reshape(B, H, W), r.gaussians(B * H * W).reshape(B, H, W)), axis=1)
+    dp = r.gaussians(B * H * W).reshape(B, H, W) * 1e-3
+    out = []
+    for fwd_bits, bwd_bits in ((1, 1), (0, 0), (1, 0), (0, 1)):
+        try:
+            _lib.call("ht_set_train_bits", fwd_bits)
+            xd = torch.from_numpy(x.astype(np.float32)).cuda()
+            p = net.forward_device(xd).double().cpu().numpy()
+            _lib.call("ht_set_train_bits", bwd_bits)
+            g = torch.zeros(net.num_params(), dtype=torch.float64, device="cuda")
+            dx = torch.zeros_like(xd)
+            net.backward_device(torch.from_numpy(dp.astype(np.float32)).cuda(), g, dx)
+            out.append((p, g.cpu().numpy(), dx.double().cpu().numpy()))
+        finally:
+            _lib.call("ht_set_train_bits", 1)
+    sizes = [q.value.size for q in net.params()]
+    offs = np.cumsum([0] + sizes)
+    p0, g0, dx0 = out[1]   # fp32 epilogue inputs throughout
+    for p, g, dx in out:
+        assert np.array_equal(p, p0)
+        assert np.linalg.norm(dx - dx0) <= 1e-6 * np.linalg.norm(dx0)
+        for k in range(len(sizes)):
+            a, b = g[offs[k]:offs[k + 1]], g0[offs[k]:offs[k + 1]]
+            assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-30, k
