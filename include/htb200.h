@@ -182,8 +182,12 @@ int ht_wgrad3x3_32(const float *x, const float *dout, int B, int H, int W, doubl
  * ResidualBlock (nn.py:91-100) and Conv2d (nn.py:46-77), fp32 math.
  * x_dev: (B, 2, H, W) float32.  act_dev: ht_train_act_bytes() bytes.
  * p_dev: (B, H, W) float32 output.  Returns HT_E_NONFINITE on non-finite
- * logits (nn.py:147-148).  The 32 -> 32 convs run on tcgen05 (split bf16),
- * the rest in fp32 SIMT (see ht_set_train_conv_impl). */
+ * logits (nn.py:147-148).  The 32 -> 32 convs run on tcgen05 (scaled fp16
+ * pairs where the shape allows TMA staging, split bf16 otherwise), the edge
+ * convs in fp32 SIMT (see ht_set_train_conv_impl).  The workspace holds the
+ * activations, three backward temporaries and the conv1 ReLU bits
+ * (ht_set_train_bits); ht_policy_backward takes the workspace its forward
+ * filled. */
 int ht_train_act_bytes(int channels, int blocks, int B, int H, int W,
                        int64_t *bytes);
 int ht_policy_forward_train(const void *packed_dev, int channels, int blocks,
