@@ -46,7 +46,7 @@ __device__ __forceinline__ double ssim3(double mx, double my, double sxx, double
 }
 
 constexpr int NMAPS = 8;
-constexpr int LE_NQ = 10;   // staged window-centre quantities of the delta kernel
+constexpr int LE_NQ = 9;    // staged window-centre quantities of the delta kernel
 constexpr int LE_SMEM = (LE_NQ * (RT + 2 * RH) * (RT + 2 * RH) + 2 * RMAXK * RMAXK) * 8;
 // RewardContext's remaining maps (metrics.py:188-204), written on request:
 //   [0] f_h  [1] f_c  [2] luminance  [3] contrast  [4] structure
@@ -194,8 +194,7 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
   constexpr int TP = RT + 2 * RH;
   // window-centre quantities around the tile, staged once per centre (each
   // centre serves up to 121 pixels): e, mu_h, shc, shh, mu_c,
-  // mu_c^2 + C1, v_c + C2, sqrt(v_c), sigma_c, SSIM (v_c = max(E[c^2] -
-  // mu_c^2, 0))
+  // mu_c^2 + C1, v_c + C2, sigma_c, SSIM (v_c = max(E[c^2] - mu_c^2, 0))
   extern __shared__ double smem_le[];
   double (*sb)[TP][TP] = reinterpret_cast<double (*)[TP][TP]>(smem_le);
   double *sk = smem_le + LE_NQ * TP * TP, *sw = sk + RMAXK * RMAXK;
@@ -217,9 +216,8 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
     sb[4][yy][xx] = muc;
     sb[5][yy][xx] = muc * muc + c1;
     sb[6][yy][xx] = vc + c2;
-    sb[7][yy][xx] = sqrt(vc);
-    sb[8][yy][xx] = in ? mb[5 * n + idx] : 0.0;   // sigma_c
-    sb[9][yy][xx] = in ? mb[6 * n + idx] : 0.0;   // SSIM before
+    sb[7][yy][xx] = in ? mb[5 * n + idx] : 0.0;   // sigma_c
+    sb[8][yy][xx] = in ? mb[6 * n + idx] : 0.0;   // SSIM before
   }
   __syncthreads();
   const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
@@ -270,15 +268,18 @@ reward_le_kernel(const T *__restrict__ m_in, const T *__restrict__ p, const T *_
         const double wd = sw[(hw + dy) * wsz + (hw + dx)];
         const int sy = ty + RH - dy, sx = tx + RH - dx;
         // SSIM_b after the edit (metrics.py:95-107 with the window sums moved
-        // by wd * (d, 2 h d + d^2, d c)), its three factors over one division
+        // by wd * (d, 2 h d + d^2, d c)).  With C3 = C2 / 2 the contrast
+        // factor's numerator is exactly twice the structure factor's
+        // denominator (2 s_h s_c + C2 = 2 (s_h s_c + C3), exact in binary
+        // floating point), so contrast x structure = 2 (cov + C3) /
+        // (v_h + v_c + C2): no square root, one division
         const double mh = sb[1][sy][sx] + wd * d;
-        const double muc = sb[4][sy][sx], syb = sb[7][sy][sx];
+        const double muc = sb[4][sy][sx];
         const double vx = fmax(sb[3][sy][sx] + wd * dh - mh * mh, 0.0);
-        const double sxv = sqrt(vx);
         const double cov = sb[2][sy][sx] + wd * dc - mh * muc;
-        const double num = (2.0 * mh * muc + c1) * (2.0 * sxv * syb + c2) * (cov + c3);
-        const double den = (mh * mh + sb[5][sy][sx]) * (vx + sb[6][sy][sx]) * (sxv * syb + c3);
-        dcs += sb[8][sy][sx] * (num / den - sb[9][sy][sx]);
+        const double num = (2.0 * mh * muc + c1) * (2.0 * (cov + c3));
+        const double den = (mh * mh + sb[5][sy][sx]) * (vx + sb[6][sy][sx]);
+        dcs += sb[7][sy][sx] * (num / den - sb[8][sy][sx]);
       }
     }
   }
