@@ -82,12 +82,56 @@ reward_maps_kernel(const T *__restrict__ p, const double *__restrict__ u,
   __shared__ double sc[RT + 2 * RH][RT + 2 * RH + 1];
   __shared__ double sk[RMAXK * RMAXK], sw[RMAXK * RMAXK];
   __shared__ double red[2][8];
+  // separable window (the reference's SSIM window is the normalised outer
+  // product of a sampled 1-D Gaussian, hvs.py:54-64): w_ij = a_i a_j with
+  // a_i = sum_j w_ij; the five window sums then take 2 x wsz products each
+  // instead of wsz^2 (horizontal pass into hs, vertical pass per pixel)
+  __shared__ double sa[RMAXK], sb1[RMAXK];
+  __shared__ double hs[5][RT + 2 * RH][RT];
+  __shared__ double hf[2][RT + 2 * RH][RT];
+  __shared__ int sep, sepk;
   const size_t n = (size_t)H * W;
   const T *pb = p + b * n;
   const double *ub = u + b * n;
   const T *cb = c + b * n;
   for (int i = threadIdx.x; i < ks * ks; i += 256) sk[i] = k[i];
   for (int i = threadIdx.x; i < wsz * wsz; i += 256) sw[i] = w[i];
+  __syncthreads();
+  // (the same for the HVS kernel k when it is a Gaussian, hvs.py:54-64; the
+  // Nasanen kernel is not separable and keeps the 2-D loop)
+  if (threadIdx.x < wsz) {
+    double r = 0.0;
+    for (int j = 0; j < wsz; ++j) r += sw[threadIdx.x * wsz + j];
+    sa[threadIdx.x] = r;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + ks) {
+    const int i = threadIdx.x - 32;
+    double r = 0.0;
+    for (int j = 0; j < ks; ++j) r += sk[i * ks + j];
+    sb1[i] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    // warp 0 checks w, warp 1 checks k: max |w_ij - a_i a_j| against max |w|
+    const bool isw = threadIdx.x < 32;
+    const int sz = isw ? wsz : ks;
+    const double *m2 = isw ? sw : sk;
+    const double *f1 = isw ? sa : sb1;
+    double mx = 0.0, err = 0.0;
+    for (int t = threadIdx.x & 31; t < sz * sz; t += 32) {
+      const double v = m2[t];
+      mx = fmax(mx, fabs(v));
+      err = fmax(err, fabs(v - f1[t / sz] * f1[t % sz]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      err = fmax(err, __shfl_xor_sync(0xffffffffu, err, o));
+    }
+    // a few ulps for the reference's Gaussians; far above for other kernels
+    if ((threadIdx.x & 31) == 0) {
+      if (isw) sep = err <= 1e-14 * mx;
+      else sepk = err <= 1e-14 * mx;
+    }
+  }
   for (int i = threadIdx.x; i < TP * TP; i += 256) {
     const int yy = i / TP, xx = i % TP;
     const int gy = y0 + yy - RH, gx = x0 + xx - RH;
@@ -107,32 +151,83 @@ reward_maps_kernel(const T *__restrict__ p, const double *__restrict__ u,
     sc[yy][xx] = cv;
   }
   __syncthreads();
+  if (sep) {
+    for (int i = threadIdx.x; i < TP * RT; i += 256) {
+      const int yy = i / RT, xx = i % RT;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+      for (int j = 0; j < wsz; ++j) {
+        const double wv = sa[j];
+        const double mv = sm[yy][xx + RH + j - hw], cv = sc[yy][xx + RH + j - hw];
+        a0 += wv * mv;
+        a1 += wv * (mv * mv);
+        a2 += wv * (mv * cv);
+        a3 += wv * cv;
+        a4 += wv * (cv * cv);
+      }
+      hs[0][yy][xx] = a0; hs[1][yy][xx] = a1; hs[2][yy][xx] = a2; hs[3][yy][xx] = a3; hs[4][yy][xx] = a4;
+    }
+  }
+  if (sepk) {
+    // convolution rows: h[yy][x] = sum_j b_j img[yy][x - (j - hk)]
+    for (int i = threadIdx.x; i < TP * RT; i += 256) {
+      const int yy = i / RT, xx = i % RT;
+      double a0 = 0.0, a1 = 0.0;
+      for (int j = 0; j < ks; ++j) {
+        const double kv = sb1[j];
+        a0 += kv * sm[yy][xx + RH - (j - hk)];
+        a1 += kv * sc[yy][xx + RH - (j - hk)];
+      }
+      hf[0][yy][xx] = a0;
+      hf[1][yy][xx] = a1;
+    }
+  }
+  if (sep || sepk) __syncthreads();
   const int tx = threadIdx.x % RT, ty = threadIdx.x / RT;
   const int gy = y0 + ty, gx = x0 + tx;
   double e2 = 0.0, cs = 0.0;
   if (gy < H && gx < W) {
     // f = conv(img, k): f[y,x] = sum_ij k[i,j] img[y-(i-hk), x-(j-hk)]
     double fh = 0.0, fc = 0.0;
-    for (int i = 0; i < ks; ++i)
-      for (int j = 0; j < ks; ++j) {
-        const double kv = sk[i * ks + j];
-        const int yy = ty + RH - (i - hk), xx = tx + RH - (j - hk);
-        fh += kv * sm[yy][xx];
-        fc += kv * sc[yy][xx];
+    if (sepk) {
+      for (int i = 0; i < ks; ++i) {
+        const double kv = sb1[i];
+        fh += kv * hf[0][ty + RH - (i - hk)][tx];
+        fc += kv * hf[1][ty + RH - (i - hk)][tx];
       }
+    } else {
+      for (int i = 0; i < ks; ++i)
+        for (int j = 0; j < ks; ++j) {
+          const double kv = sk[i * ks + j];
+          const int yy = ty + RH - (i - hk), xx = tx + RH - (j - hk);
+          fh += kv * sm[yy][xx];
+          fc += kv * sc[yy][xx];
+        }
+    }
     // window sums by correlation with w
     double muh = 0.0, shc = 0.0, muc = 0.0, scc = 0.0, shh = 0.0;
-    for (int i = 0; i < wsz; ++i)
-      for (int j = 0; j < wsz; ++j) {
-        const double wv = sw[i * wsz + j];
-        const int yy = ty + RH + i - hw, xx = tx + RH + j - hw;
-        const double mv = sm[yy][xx], cv = sc[yy][xx];
-        muh += wv * mv;
-        shh += wv * (mv * mv);
-        shc += wv * (mv * cv);
-        muc += wv * cv;
-        scc += wv * (cv * cv);
+    if (sep) {
+      for (int i = 0; i < wsz; ++i) {
+        const double wv = sa[i];
+        const int yy = ty + RH + i - hw;
+        muh += wv * hs[0][yy][tx];
+        shh += wv * hs[1][yy][tx];
+        shc += wv * hs[2][yy][tx];
+        muc += wv * hs[3][yy][tx];
+        scc += wv * hs[4][yy][tx];
       }
+    } else {
+      for (int i = 0; i < wsz; ++i)
+        for (int j = 0; j < wsz; ++j) {
+          const double wv = sw[i * wsz + j];
+          const int yy = ty + RH + i - hw, xx = tx + RH + j - hw;
+          const double mv = sm[yy][xx], cv = sc[yy][xx];
+          muh += wv * mv;
+          shh += wv * (mv * mv);
+          shc += wv * (mv * cv);
+          muc += wv * cv;
+          scc += wv * (cv * cv);
+        }
+    }
     const double sig = fmin(gain * sqrt(fmax(scc - muc * muc, 0.0)), 1.0);
     double parts[3];
     const double s = ssim3(muh, muc, shh, scc, shc, c1, c2, parts);

@@ -139,3 +139,47 @@ def test_policy_network_other_in_channels():
     net.conv_out.bias.value[0] = np.inf
     with pytest.raises(FloatingPointError):
         net.forward(x)
+
+
+@pytest.mark.parametrize("separable", [True, False])
+def test_reward_maps_any_window_against_oracle(separable):
+    """The reward-map kernel takes the separable path (2 x 11 products per
+    window sum) only when the stencils are outer products (the reference's
+    Gaussians, hvs.py:54-64) and the 2-D loop otherwise: both against the
+    oracle's RewardContext / delta_map with the same stencils (float64)."""
+    import torch
+    from oracle import htoracle as O
+    from paper_2304_12152_b200 import _lib
+    rs = np.random.default_rng(3)
+    H, W = 37, 45
+    h = (rs.random((H, W)) < 0.5).astype(np.float64)
+    c = rs.random((H, W))
+    if separable:
+        k, w = O.gaussian_kernel(11, 2.0), O.gaussian_kernel(11, 1.5)
+    else:
+        k = rs.random((9, 9)); k /= k.sum()
+        w = rs.random((11, 11)); w /= w.sum()
+    ref = O.RewardMaps(h, c, k, w)
+    dev = torch.device("cuda")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev)   # noqa: E731
+    hd, cd, kd, wd = t(h)[None], t(c)[None], t(k), t(w)
+    maps = torch.empty((1, 8, H, W), dtype=torch.float64, device=dev)
+    extra = torch.empty((1, 7, H, W), dtype=torch.float64, device=dev)
+    sums = torch.empty((1, 2), dtype=torch.float64, device=dev)
+    scratch = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+    _lib.call("ht_reward_context_f64", _lib.ptr(hd), _lib.ptr(cd), 1, H, W, _lib.ptr(kd), k.shape[0],
+              _lib.ptr(wd), w.shape[0], 0.06, 1e-4, 9e-4, 2.0, _lib.ptr(maps), _lib.ptr(extra),
+              _lib.ptr(sums), _lib.ptr(scratch), 0)
+    m = maps[0].cpu().numpy()
+    for got, want in ((m[0], ref.e), (m[1], ref.mu_h), (m[2], ref.shc), (m[3], ref.mu_c), (m[4], ref.scc),
+                      (m[5], ref.sigma_c), (m[6], ref.ssim), (m[7], ref.shh)):
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-14)
+    other = 1.0 - h
+    od = t(other)[None]
+    out = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+    nbytes = _lib.out_i64("ht_reward_workspace_bytes", 1, H, W) + 8 * H * W
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _lib.call("ht_reward_delta_f64", _lib.ptr(hd), _lib.ptr(od), _lib.ptr(cd), 1, H, W, _lib.ptr(kd), k.shape[0],
+              _lib.ptr(wd), w.shape[0], 0.06, 1e-4, 9e-4, 2.0, _lib.ptr(out), _lib.ptr(ws), nbytes, 0)
+    d_ref = ref.delta_map(other)
+    assert np.allclose(out[0].cpu().numpy(), d_ref, rtol=1e-9, atol=1e-15 * np.abs(d_ref).max())
