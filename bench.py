@@ -356,22 +356,27 @@ def bench_cfg1(D, net, reps):
             e1.record(st)
             torch.cuda.synchronize()
             dev_ms.append(e0.elapsed_time(e1))
-        eng = rl.HalftoneEngine(net, 1, 256, 256, chunks=1, output="h", depth=1)
         ch, zh = c.cpu().pin_memory(), z.cpu().pin_memory()
-        oh = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
-        e2e_ms = []
-        for _ in range(reps + 3):
-            l2_flush(dev)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            eng(ch, zh, oh)
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    assert torch.equal(oh, h.cpu()), "cfg1: e2e output differs from the device path"
+        e2e = {}
+        for mode in ("graph", "streams"):
+            eng = rl.HalftoneEngine(net, 1, 256, 256, chunks=1, output="h", depth=1,
+                                    graph=mode == "graph")
+            oh = torch.empty(eng.out_shape(), dtype=torch.uint8).pin_memory()
+            e2e[mode] = []
+            for _ in range(reps + 3):
+                l2_flush(dev)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                eng(ch, zh, oh)
+                e2e[mode].append((time.perf_counter() - t0) * 1e3)
+            assert torch.equal(oh, h.cpu()), f"cfg1: e2e ({mode}) output differs from the device path"
+    e2e_ms = e2e["graph"]
     return {"workload": "BASELINE config 1: 1 x 256x256 contone (seed 0), batch 1",
             "latency_ms": round(float(np.median(dev_ms[3:])), 4),
             "latency_ms_e2e": round(float(np.median(e2e_ms[3:])), 4),
+            "latency_ms_e2e_streams": round(float(np.median(e2e["streams"][3:])), 4),
             "unit": "ms (median, L2 flushed before each run)", "reps": reps,
-            "e2e_api": "rl.HalftoneEngine(B=1) pinned host fp32 in -> uint8 out, wall clock",
+            "e2e_api": "rl.HalftoneEngine(B=1, graph=True) pinned host fp32 in -> uint8 out, one CUDA-graph replay (H2D, 9 K1 passes, D2H, flag), wall clock; _streams = the same engine without the graph",
             "clocks": clk.summary()}
 
 

@@ -269,6 +269,9 @@ class PolicyNetwork:
     def _repack(self):
         _lib.call("ht_pack_params", _lib.ptr(self._flat), self.channels, self.blocks,
                   _lib.ptr(self._packed), _lib.stream_ptr())
+        # counts repacks (host uploads and device updates alike): captured
+        # CUDA graphs that baked in the biases compare it (rl.HalftoneEngine)
+        self.upload_generation = getattr(self, "upload_generation", 0) + 1
 
     def device_flat(self):
         self.sync()

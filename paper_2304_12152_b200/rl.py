@@ -733,7 +733,7 @@ class HalftoneEngine:
     `depth` sets of device buffers: batch i+1's copies overlap batch i's
     kernels, and one chunk per batch keeps the launches few."""
 
-    def __init__(self, net, B, H, W, chunks=4, output="h", impl=None, depth=2):
+    def __init__(self, net, B, H, W, chunks=4, output="h", impl=None, depth=2, graph=False):
         torch = _torch()
         _lib.require_cuda()
         if output not in ("h", "pbm", "p"):
@@ -773,6 +773,13 @@ class HalftoneEngine:
                 "out": out, "ws": [None, None]})
         self._next = 0
         self.out = self._sets[0]["out"]
+        # graph=True (latency mode): a call with pinned host tensors replays
+        # one CUDA graph of H2D -> fused forward -> D2H (+ the non-finite
+        # flag's 4 bytes), captured per (host buffers, parameter upload)
+        self.graph = graph
+        self._graph = None
+        self._graph_key = None
+        self._flag_host = torch.zeros(1, dtype=torch.int32, pin_memory=True) if graph else None
         net.sync()
 
     def out_shape(self):
@@ -791,8 +798,58 @@ class HalftoneEngine:
         in image order, as B calls of rl.infer_halftone would draw it
         (rl.py:306-311); out_host: CPU tensor shaped out_shape().  Returns
         out_host once it holds the result."""
+        if (self.graph and not isinstance(z_host, Rng) and c_host.is_pinned()
+                and z_host.is_pinned() and out_host.is_pinned()):
+            return self._graph_call(c_host, z_host, out_host)
         self.wait(self.submit(c_host, z_host, out_host))
         return out_host
+
+    def _graph_call(self, c_host, z_host, out_host):
+        """One batch as a single CUDA-graph replay on the current stream (the
+        nine K1 passes keep their programmatic-dependent edges inside the
+        graph); the host waits once and reads the flag copied by the graph."""
+        torch = _torch()
+        self.net.sync()
+        # the graph bakes in the host buffers and the per-pass biases (kernel
+        # parameters): any other buffer or a newer parameter upload recaptures
+        key = (c_host.data_ptr(), z_host.data_ptr(), out_host.data_ptr(),
+               getattr(self.net, "upload_generation", 0))
+        if self._graph is None or self._graph_key != key:
+            self._capture(c_host, z_host, out_host, key)
+        cur = torch.cuda.current_stream(self.dev)
+        self._graph.replay()
+        cur.synchronize()
+        if int(self._flag_host[0]) != 0:
+            raise FloatingPointError("non-finite logits in the fused forward (use impl=1 or "
+                                     "rl.halftone for networks that leave fp16's range)")
+        return out_host
+
+    def _capture(self, c_host, z_host, out_host, key):
+        torch = _torch()
+        st = self._sets[0]
+        cbuf, zbuf, obuf = st["c"], st["z"], st["out"]
+        kw = {"h_out" if self.output == "h" else
+              ("pbm_out" if self.output == "pbm" else "p_out"): obuf}
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        # uncaptured run first: allocates the workspace, sets the kernels'
+        # shared-memory attributes and refreshes the library's host bias copy
+        with torch.cuda.stream(s):
+            cbuf.copy_(c_host, non_blocking=True)
+            zbuf.copy_(z_host, non_blocking=True)
+            ws = self.net.halftone_device(cbuf, zbuf, impl=self.impl, workspace=st["ws"][0],
+                                          stream=s, **kw)
+        s.synchronize()
+        st["ws"][0] = ws
+        self._graph = None
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            cbuf.copy_(c_host, non_blocking=True)
+            zbuf.copy_(z_host, non_blocking=True)
+            self.net.halftone_device(cbuf, zbuf, impl=self.impl, workspace=ws, stream=s, **kw)
+            out_host.copy_(obuf, non_blocking=True)
+            self._flag_host.copy_(ws[:4].view(torch.int32), non_blocking=True)
+        self._graph, self._graph_key = g, key
 
     def submit(self, c_host, z_host, out_host):
         """Enqueue one batch (H2D -> fused forward -> D2H) without waiting and

@@ -336,6 +336,42 @@ def test_engine_streamed_batches_equal_sequential_calls(noise):
         assert rs2.state_words() == rs.state_words()
 
 
+@pytest.mark.parametrize("output", ["h", "pbm", "p"])
+def test_engine_graph_mode_equals_streamed_path(output):
+    """HalftoneEngine(graph=True): the call replays one captured CUDA graph
+    (H2D, the nine K1 passes, D2H) and gives exactly the streamed path's
+    result; new host buffers or an edited parameter force a recapture, and a
+    non-finite logit still raises."""
+    import torch
+    from paper_2304_12152_b200 import rl
+    from paper_2304_12152_b200.imagecore import Rng
+    net = _net(0.05)
+    B, H, W = 2, 40, 72
+    r = Rng(5)
+    mk = lambda f: torch.from_numpy(f(B * H * W).reshape(B, H, W).astype(np.float32)).pin_memory()
+    c, z = mk(r.uniforms), mk(r.gaussians_f32)
+    ref_eng = rl.HalftoneEngine(net, B, H, W, chunks=1, output=output, depth=1)
+    eng = rl.HalftoneEngine(net, B, H, W, output=output, depth=1, graph=True)
+    dt = ref_eng.out.dtype
+    ref = ref_eng(c, z, torch.empty(ref_eng.out_shape(), dtype=dt).pin_memory()).clone()
+    o = torch.empty(eng.out_shape(), dtype=dt).pin_memory()
+    for _ in range(3):
+        o.zero_()
+        assert torch.equal(eng(c, z, o), ref)
+    g0 = eng._graph
+    c.copy_(mk(r.uniforms))                      # same buffers, new contents: same graph
+    ref = ref_eng(c, z, torch.empty_like(ref)).clone()
+    assert torch.equal(eng(c, z, o), ref) and eng._graph is g0
+    net.conv_out.bias.value[0] += 0.5            # edited parameter: recaptured
+    ref = ref_eng(c, z, torch.empty_like(ref)).clone()
+    assert torch.equal(eng(c, z, o), ref) and eng._graph is not g0
+    o2 = torch.empty_like(o)                     # other host buffers: recaptured
+    assert torch.equal(eng(c, z, o2), ref)
+    c[0, 3, 5] = float("nan")
+    with pytest.raises(FloatingPointError):
+        eng(c, z, o2)
+
+
 @pytest.mark.parametrize("case", ["trained_2k", "std0.1"])
 def test_config1_beyond_random_init(case):
     """K1 parity with weights that are not the std-0.01 init: the network
